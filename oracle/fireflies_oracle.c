@@ -1,0 +1,260 @@
+/* fireflies_oracle.c -- the CPU oracle for the Fireflies hot path (arXiv:1505.00344).
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library. The product path
+ * (paper_1505_00344_b200/) never imports, links or calls anything under oracle/.
+ *
+ * Independence: this file shares no code, header, table or constant generator with the
+ * CUDA path. It has its own hand-coded right-hand sides (oracle_impl.h), its own
+ * Philox4x32-10, its own initial-condition formula and its own projection / binning.
+ *
+ * Build (see oracle/build.py): gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fopenmp
+ * -shared -fPIC. FP contraction is off and fast-math is off, so every float operation is one
+ * IEEE-754 round-to-nearest operation in program order (x86-64 SSE, no x87 excess precision).
+ *
+ * What is pinned (tests/test_oracle_*.py) and what is not -- see DESIGN.md "Oracle":
+ *   rk4 (all models)       pinned: closed forms (linear, harmonic), order-4 convergence,
+ *                          round trip, fixed points
+ *   rhs_lorenz             pinned: PAPER.md:87-93 landmarks, analytic fixed points, rhs(1,1,1)
+ *   rhs_hh                 pinned: textbook m,h,n steady states, rest 0 mV,
+ *                          onset of repetitive firing ~6.25
+ *   rhs_stn                pinned by special cases (w = 0 closed form, forward invariance of
+ *                          (0,1)^2 per PAPER.md:40); the sigmoid constants themselves are
+ *                          unpublished -> "parity unpinned" for their values (reading R6)
+ *   philox4x32_10          pinned: Random123 known-answer vectors
+ *   ic / sweep / project   pinned: bin-centre placement, edge rules, brute force, golden pixels
+ *
+ * Model ids and parameter vectors:
+ *   ORC_LINEAR   (0) dim d, p = A (d*d, row-major)
+ *   ORC_HARMONIC (1) dim 2, p = {omega}
+ *   ORC_LORENZ   (2) dim 3, p = {sigma, r, beta}
+ *   ORC_STN      (3) dim 2, p = {w_ss, w_gs, w_sg, w_gg, I, tau_s, tau_g,
+ *                               a_s, theta_s, a_g, theta_g}
+ *   ORC_HH       (4) dim 5N, p = {C, g_na, g_k, g_lk, e_na, e_k, e_lk, g_syn, e_syn,
+ *                                 tau_r, tau_d, sigma, theta, I_1..I_N}
+ */
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#define ORC_LINEAR 0
+#define ORC_HARMONIC 1
+#define ORC_LORENZ 2
+#define ORC_STN 3
+#define ORC_HH 4
+#define ORC_MAX_DIM 64
+#define ORC_MAX_PARAMS 128
+
+/* ---- float instantiation ---- */
+#define REAL float
+#define SFX _f32
+#define EXP expf
+#define FABS fabsf
+#include "oracle_impl.h"
+#undef REAL
+#undef SFX
+#undef EXP
+#undef FABS
+
+/* ---- double instantiation ---- */
+#define REAL double
+#define SFX _f64
+#define EXP exp
+#define FABS fabs
+#include "oracle_impl.h"
+#undef REAL
+#undef SFX
+#undef EXP
+#undef FABS
+
+/* =====================================================================================
+ * Philox4x32-10 (Salmon et al., SC'11, "Parallel random numbers: as easy as 1, 2, 3";
+ * the Random123 reference definition). The paper names no generator (PAPER.md:42 says only
+ * "uniform random distribution"); reading R5 fixes Philox4x32-10.
+ *   round: (L0, R0, L1, R1) = (c0, c1, c2, c3)
+ *     hi0:lo0 = M0 * c0,  hi1:lo1 = M1 * c2
+ *     c' = (hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0)
+ *   key bump after each of the first 9 rounds: k0 += W0, k1 += W1.
+ * ===================================================================================== */
+#define PHILOX_M0 0xD2511F53u
+#define PHILOX_M1 0xCD9E8D57u
+#define PHILOX_W0 0x9E3779B9u
+#define PHILOX_W1 0xBB67AE85u
+
+void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+  uint32_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+  uint32_t k0 = key_in[0], k1 = key_in[1];
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += PHILOX_W0; k1 += PHILOX_W1; }
+    const uint64_t p0 = (uint64_t)PHILOX_M0 * c[0];
+    const uint64_t p1 = (uint64_t)PHILOX_M1 * c[2];
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n1 = lo1, n2 = hi0 ^ c[3] ^ k1, n3 = lo0;
+    c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+  }
+  out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
+}
+
+/* Uniform float in [0,1) from one 32-bit word: u = (r >> 8) * 2^-24 (exact in float). */
+static float u01_from_word(uint32_t r) { return (float)(r >> 8) * 0x1p-24f; }
+
+/* The largest float strictly below hi (hi finite). */
+static float float_below(float hi) { return nextafterf(hi, -INFINITY); }
+
+/* One uniform sample in [lo, hi) per DESIGN.md reading R5:
+ *   x = lo + (hi - lo) * u   (three IEEE float ops, in this order)
+ *   x = min(x, largest float below hi)   (rounding can otherwise reach hi). */
+static float uniform_in_box(float lo, float hi, float u) {
+  const float w = hi - lo;
+  const float t = w * u;
+  float x = lo + t;
+  const float top = float_below(hi);
+  if (x > top) x = top;
+  return x;
+}
+
+/* Philox counter layout of DESIGN.md reading R5 (initial conditions of PAPER.md:42, :207):
+ *   key = {seed lo32, seed hi32}
+ *   ctr = {i lo32, i hi32, d / 4, stream}   i = particle index inside its group
+ *   word = d % 4                             stream 0 = IC, 1 = swept parameter */
+static uint32_t philox_word(uint64_t seed, uint64_t i, uint32_t block, uint32_t stream, int word) {
+  const uint32_t ctr[4] = {(uint32_t)i, (uint32_t)(i >> 32), block, stream};
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t out[4];
+  orc_philox4x32_10(ctr, key, out);
+  return out[word];
+}
+
+/* Public: initial conditions for particles first .. first+count-1 of one group whose IC cube
+ * is [lo_d, hi_d) per dimension. Output SoA: out[d*pitch + j] for the j-th particle. */
+int orc_ic_uniform_f32(const float* lo, const float* hi, int dim, uint64_t seed, int64_t first,
+                       int64_t count, float* out, int64_t pitch) {
+  if (dim < 1 || count < 0 || first < 0 || pitch < count) return -1;
+  for (int d = 0; d < dim; ++d)
+    if (!(lo[d] < hi[d]) || !isfinite(lo[d]) || !isfinite(hi[d])) return -1;
+  for (int64_t j = 0; j < count; ++j) {
+    const uint64_t i = (uint64_t)(first + j);
+    for (int d = 0; d < dim; ++d) {
+      const uint32_t r = philox_word(seed, i, (uint32_t)(d / 4), 0u, d % 4);
+      out[(int64_t)d * pitch + j] = uniform_in_box(lo[d], hi[d], u01_from_word(r));
+    }
+  }
+  return 0;
+}
+
+/* Public: swept-parameter values (each particle has its own fixed value).
+ * mode 0: Philox-uniform in [lo, hi) (stream 1, block 0, word 0);
+ * mode 1: linspace, v_i = lo + (hi - lo) * ((i + 0.5) / n_group), computed as
+ *         t = (float)(i + 0.5) / (float)n_group ... see DESIGN.md reading R13 for the exact ops. */
+int orc_sweep_values_f32(float lo, float hi, int mode, uint64_t seed, int64_t first, int64_t count,
+                         int64_t n_group, float* out) {
+  if (!(lo < hi) || count < 0 || first < 0 || n_group < 1 || first + count > n_group) return -1;
+  for (int64_t j = 0; j < count; ++j) {
+    const uint64_t i = (uint64_t)(first + j);
+    if (mode == 0) {
+      out[j] = uniform_in_box(lo, hi, u01_from_word(philox_word(seed, i, 0u, 1u, 0)));
+    } else if (mode == 1) {
+      /* (i + 0.5) / n in double (exact numerator for i < 2^52), rounded once to float. */
+      const float u = (float)(((double)i + 0.5) / (double)n_group);
+      out[j] = uniform_in_box(lo, hi, u);
+    } else {
+      return -1;
+    }
+  }
+  return 0;
+}
+
+/* =====================================================================================
+ * Projection + density histogram (readings R17-R19).
+ * Axis values v_k are picked from the "extended state" = the dim state components followed
+ * by the swept value (index dim). Each particle adds 1 to image[colour][iy][ix] if it lands
+ * in the window; everything else (non-finite, outside, behind the camera) is dropped.
+ *
+ * 2-D (n_axes = 2), view = {lo_0, hi_0, lo_1, hi_1}:
+ *   keep iff lo_k <= v_k < hi_k for k = 0, 1
+ *   s_0 = (float)W / (hi_0 - lo_0), s_1 = (float)H / (hi_1 - lo_1)     (IEEE float ops)
+ *   ix = min(floor((v_0 - lo_0) * s_0), W - 1), iy likewise with H
+ * 3-D (n_axes = 3), view = row-major 4x4 M (view-projection):
+ *   c_r = ((M[r][0] a + M[r][1] b) + M[r][2] c) + M[r][3]   for r = 0 (x), 1 (y), 3 (w);
+ *   every product and sum rounded separately, in that order
+ *   keep iff c_w > 0;  px = (c_0 / c_w + 1) * (W * 0.5),  py = (c_1 / c_w + 1) * (H * 0.5)
+ *   keep iff 0 <= px < W and 0 <= py < H;  ix = floor(px), iy = floor(py)
+ * ===================================================================================== */
+static int64_t bin_2d(const float* v, const float* view, int W, int H) {
+  const float lo0 = view[0], hi0 = view[1], lo1 = view[2], hi1 = view[3];
+  if (!(v[0] >= lo0 && v[0] < hi0)) return -1;
+  if (!(v[1] >= lo1 && v[1] < hi1)) return -1;
+  const float s0 = (float)W / (hi0 - lo0);
+  const float s1 = (float)H / (hi1 - lo1);
+  const float px = (v[0] - lo0) * s0;
+  const float py = (v[1] - lo1) * s1;
+  int64_t ix = (int64_t)floorf(px), iy = (int64_t)floorf(py);
+  if (ix > W - 1) ix = W - 1;
+  if (iy > H - 1) iy = H - 1;
+  return iy * (int64_t)W + ix;
+}
+
+static float mat_row(const float* M, int r, float a, float b, float c) {
+  float acc = M[4 * r + 0] * a;
+  const float t1 = M[4 * r + 1] * b;
+  acc = acc + t1;
+  const float t2 = M[4 * r + 2] * c;
+  acc = acc + t2;
+  acc = acc + M[4 * r + 3];
+  return acc;
+}
+
+static int64_t bin_3d(const float* v, const float* M, int W, int H) {
+  const float cx = mat_row(M, 0, v[0], v[1], v[2]);
+  const float cy = mat_row(M, 1, v[0], v[1], v[2]);
+  const float cw = mat_row(M, 3, v[0], v[1], v[2]);
+  if (!(cw > 0.0f)) return -1;
+  const float nx = cx / cw, ny = cy / cw;
+  const float px = (nx + 1.0f) * ((float)W * 0.5f);
+  const float py = (ny + 1.0f) * ((float)H * 0.5f);
+  if (!(px >= 0.0f && px < (float)W)) return -1;
+  if (!(py >= 0.0f && py < (float)H)) return -1;
+  const int64_t ix = (int64_t)floorf(px), iy = (int64_t)floorf(py);
+  return iy * (int64_t)W + ix;
+}
+
+/* Public: bin index (iy*W + ix, within one channel) of each particle, or -1 if dropped. */
+int orc_bin_f32(const float* x_soa, int64_t n, int64_t pitch, int dim, const float* sweep_vals,
+                const int* axes, int n_axes, const float* view, int W, int H, int64_t* bins) {
+  if (n_axes != 2 && n_axes != 3) return -1;
+  if (W < 1 || H < 1 || n < 0) return -1;
+  for (int k = 0; k < n_axes; ++k) {
+    if (axes[k] < 0 || axes[k] > dim) return -1;
+    if (axes[k] == dim && !sweep_vals) return -1;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    float v[3];
+    for (int k = 0; k < n_axes; ++k)
+      v[k] = (axes[k] == dim) ? sweep_vals[i] : x_soa[(int64_t)axes[k] * pitch + i];
+    bins[i] = (n_axes == 2) ? bin_2d(v, view, W, H) : bin_3d(v, view, W, H);
+  }
+  return 0;
+}
+
+/* Public: add 1 to image[colour][bin] for every kept particle (image is C*H*W uint32,
+ * caller-initialised; additive blending analogue of PAPER.md:236). */
+int orc_histogram_f32(const float* x_soa, int64_t n, int64_t pitch, int dim, const float* sweep_vals,
+                      const int* axes, int n_axes, const float* view, int W, int H, int C, int colour,
+                      uint32_t* image) {
+  if (colour < 0 || colour >= C) return -1;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t b;
+    float v[3];
+    if (n_axes != 2 && n_axes != 3) return -1;
+    for (int k = 0; k < n_axes; ++k) {
+      if (axes[k] < 0 || axes[k] > dim || (axes[k] == dim && !sweep_vals)) return -1;
+      v[k] = (axes[k] == dim) ? sweep_vals[i] : x_soa[(int64_t)axes[k] * pitch + i];
+    }
+    b = (n_axes == 2) ? bin_2d(v, view, W, H) : bin_3d(v, view, W, H);
+    if (b >= 0) image[(int64_t)colour * H * W + b] += 1u;
+  }
+  return 0;
+}
+
+int orc_version(void) { return 1; }

@@ -1,0 +1,261 @@
+"""Pins of the oracle's hand-coded right-hand sides against what the paper states and what the
+mathematics of each model fixes (no GPU)."""
+import json
+import os
+
+import numpy as np
+import pytest
+from scipy.special import expit
+
+import oracle as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+LORENZ_P = [10.0, 28.0, 8.0 / 3.0]
+
+
+def lorenz_box(n, seed):
+    rng = np.random.default_rng(seed)
+    # Fig. 3A IC box.
+    return np.vstack([rng.uniform(-10, 10, n), rng.uniform(-30, 30, n), rng.uniform(0, 50, n)])
+
+
+# ----------------------------------------------------------------------------- Lorenz
+def test_lorenz_rhs_hand_value():
+    # rhs(1,1,1) with sigma=10, r=28, beta=8/3 is (0, 26, -5/3) -- direct
+    # substitution into PAPER.md Eqs. 3-5.
+    np.testing.assert_allclose(O.rhs(O.LORENZ, [1, 1, 1], LORENZ_P), [0, 26, -5 / 3], atol=1e-14)
+
+
+@pytest.mark.parametrize("r", [5.0, 15.0, 28.0])
+def test_lorenz_fixed_points_closed_form(r):
+    # C+- = (+-sqrt(beta (r-1)), +-sqrt(beta (r-1)), r-1) solve f = 0 (Strogatz, cited at PAPER.md:79).
+    b = 8.0 / 3.0
+    q = np.sqrt(b * (r - 1))
+    for s in (1, -1):
+        dx = O.rhs(O.LORENZ, [s * q, s * q, r - 1], [10.0, r, b])
+        assert np.max(np.abs(dx)) < 1e-12
+
+
+def test_lorenz_golden_values():
+    g = json.load(open(os.path.join(GOLD, "lorenz_golden.json")))
+    for c in g["cases"]:
+        p = [g["sigma"], c["r"], g["beta_num"] / g["beta_den"]]
+        x = O.rk4(O.LORENZ, np.array(g["x0"])[:, None], p, g["dt"], c["steps"])[:, 0]
+        np.testing.assert_allclose(x, c["x"], rtol=g["rtol"], atol=1e-15)
+
+
+def test_lorenz_r_below_one_collapses_to_origin():
+    # PAPER.md:87 "For values of r less than 1, the origin is the only stable fixed point";
+    # >= 99% within 1e-2 of the origin at t=50.
+    x = O.rk4(O.LORENZ, lorenz_box(2000, 10), [10.0, 0.5, 8 / 3], 0.01, 5000)
+    d = np.linalg.norm(x, axis=0)
+    assert np.mean(d < 1e-2) >= 0.99
+
+
+def test_lorenz_r5_two_stable_fixed_points():
+    # past the pitchfork at r=1 two new stable fixed points; at r=5 every particle
+    # ends at one of C+- (SPEC.md:485).
+    r, b = 5.0, 8.0 / 3.0
+    q = np.sqrt(b * (r - 1))
+    x = O.rk4(O.LORENZ, lorenz_box(500, 11), [10.0, r, b], 0.01, 10000)
+    dp = np.linalg.norm(x - np.array([[q], [q], [r - 1]]), axis=0)
+    dm = np.linalg.norm(x - np.array([[-q], [-q], [r - 1]]), axis=0)
+    assert np.all(np.minimum(dp, dm) < 1e-2)
+    assert np.any(dp < 1e-2) and np.any(dm < 1e-2)
+
+
+def test_lorenz_r28_bounded_attractor():
+    # PAPER.md:93 strange attractor; bounded |x|,|y| < 30, 0 < z < 60 over t in [20, 40].
+    x = O.rk4(O.LORENZ, lorenz_box(300, 12), LORENZ_P, 0.01, 2000)
+    ok = np.ones(x.shape[1], bool)
+    for _ in range(20):
+        x = O.rk4(O.LORENZ, x, LORENZ_P, 0.01, 100)
+        ok &= (np.abs(x[0]) < 30) & (np.abs(x[1]) < 30) & (x[2] > 0) & (x[2] < 60)
+    assert ok.mean() >= 0.99
+
+
+def test_lorenz_spirals_stable_below_hopf_unstable_above():
+    # C+- remain stable until r ~ 24.74 (= sigma(sigma+beta+3)/(sigma-beta-1)).
+    b = 8.0 / 3.0
+    assert 10 * (10 + b + 3) / (10 - b - 1) == pytest.approx(24.74, abs=5e-3)
+    for r, stable in ((22.0, True), (27.0, False)):
+        q = np.sqrt(b * (r - 1))
+        c = np.array([[q], [q], [r - 1]])
+        x = O.rk4(O.LORENZ, c + 1e-3, [10.0, r, b], 0.01, 3000)
+        d = np.linalg.norm(x - c)
+        assert (d < 1e-3) == stable
+
+
+# ----------------------------------------------------------------------------- HH
+HH_DEFAULTS = dict(C=1.0, g_na=120.0, g_k=36.0, g_lk=0.3, e_na=115.0, e_k=-12.0, e_lk=10.613,
+                   g_syn=0.5, e_syn=10.0, tau_r=0.5, tau_d=3.0, sigma=5.0, theta=20.0)
+
+
+def hh_p(n, **kw):
+    d = dict(HH_DEFAULTS)
+    d.update({f"I{i + 1}": 10.0 for i in range(n)})
+    d.update(kw)
+    return np.array([d[k] for k in O.hh_param_names(n)])
+
+
+def test_hh_gate_steady_states_textbook():
+    # Textbook HH gate values at rest (V = 0): m 0.0529, h 0.5961, n 0.3177.
+    gold = json.load(open(os.path.join(GOLD, "paper_values.json")))["hh"]["textbook_gates_at_rest"]
+    p = hh_p(1, g_syn=0.0, I1=0.0)
+    for k, idx in (("h", 1), ("m", 2), ("n", 3)):
+        lo, hi = 0.0, 1.0  # bisection on the gate's derivative, which is decreasing in the gate
+        for _ in range(60):
+            mid = (lo + hi) / 2
+            x = [0.0, 0.5, 0.5, 0.5, 0.0]
+            x[idx] = mid
+            if O.rhs(O.HH, x, p)[idx] > 0:
+                lo = mid
+            else:
+                hi = mid
+        assert lo == pytest.approx(gold[k], abs=6e-5)
+
+
+def test_hh_rest_potential_zero():
+    # with I = I_syn = 0 the membrane approaches a fixed point at 0 mV.
+    x0 = np.array([[5.0], [0.6], [0.05], [0.32], [0.0]])
+    x = O.rk4(O.HH, x0, hh_p(1, g_syn=0.0, I1=0.0), 0.01, 20000)
+    assert abs(x[0, 0]) < 0.05
+
+
+def _count_spikes(x, p, steps, dt=0.01, every=10):
+    cnt = np.zeros(x.shape[1])
+    times = [[] for _ in range(x.shape[1])]
+    prev = x[0].copy()
+    for k in range(steps // every):
+        x = O.rk4(O.HH, x, p, dt, every)
+        up = (prev < 20) & (x[0] >= 20)
+        cnt += up
+        for i in np.nonzero(up)[0]:
+            times[i].append((k + 1) * every * dt)
+        prev = x[0].copy()
+    return x, cnt, times
+
+
+def test_hh_onset_of_repetitive_firing_near_6_25():
+    # "As I_1 is increased past I_1 ~ 6.25 ... a stable limit cycle appears".
+    rng = np.random.default_rng(20)
+    n = 128
+    x0 = np.vstack([rng.uniform(-20, 100, n), rng.uniform(0, 1, (4, n))])
+    counts = {}
+    for I in (6.2, 6.3):
+        p = hh_p(1, g_syn=0.0, I1=I)
+        x = O.rk4(O.HH, x0, p, 0.01, 20000)
+        _, cnt, _ = _count_spikes(x, p, 10000)
+        counts[I] = cnt
+    assert np.all(counts[6.2] == 0)
+    assert np.mean(counts[6.3] >= 3) > 0.5
+
+
+def test_hh_period_at_I10():
+    # Repetitive firing at I = 10; period 14.64 ms (SURVEY.md:507, independent
+    # computation), inter-spike-interval CV < 5%.
+    p = hh_p(1, g_syn=0.0, I1=10.0)
+    x = O.rk4(O.HH, np.array([[0.0], [0.596], [0.053], [0.318], [0.0]]), p, 0.01, 10000)
+    _, cnt, times = _count_spikes(x, p, 20000, every=1)
+    isi = np.diff(times[0])
+    assert cnt[0] >= 5
+    assert np.mean(isi) == pytest.approx(14.64, abs=0.05)
+    assert np.std(isi) / np.mean(isi) < 0.05
+
+
+def test_hh_ring_index_wraps():
+    # PAPER.md:133, reading R9: neuron 1 receives s of neuron N. With only s_N nonzero, only
+    # neuron 1's V derivative changes when g_syn changes.
+    n = 3
+    x = np.array([0.0, 0.6, 0.05, 0.32, 0.0] * n)
+    x[5 * (n - 1) + 4] = 0.8
+    a = O.rhs(O.HH, x, hh_p(n, g_syn=0.0))
+    b = O.rhs(O.HH, x, hh_p(n, g_syn=0.5))
+    dv = b[0::5] - a[0::5]
+    assert dv[0] == pytest.approx(0.5 * (10.0 - 0.0) * 0.8)
+    assert dv[1] == 0 and dv[2] == 0
+
+
+def test_hh_ring_synchronises():
+    # "a very stable synchronous state"; > 50% of random-IC
+    # particles synchronous (max pairwise |V_i - V_j| < 5 mV over a period) after t = 500 ms.
+    rng = np.random.default_rng(21)
+    n = 96
+    x0 = np.vstack([np.vstack([rng.uniform(-20, 100, n), rng.uniform(0, 1, (4, n))]) for _ in range(3)])
+    p = hh_p(3)
+    x = O.rk4(O.HH, x0, p, 0.01, 50000)
+    worst = np.zeros(n)
+    for _ in range(150):
+        x = O.rk4(O.HH, x, p, 0.01, 10)
+        V = x[0::5]
+        worst = np.maximum(worst, V.max(axis=0) - V.min(axis=0))
+    assert np.mean(worst < 5.0) > 0.5
+
+
+# ----------------------------------------------------------------------------- STN-GPe
+STN_DEFAULTS = dict(w_ss=0.0, w_gs=8.971, w_sg=15.168, w_gg=8.502, I=2.216, tau_s=1.0, tau_g=2.77,
+                    a_s=2.891, theta_s=2.049, a_g=1.826, theta_g=2.032)
+
+
+def stn_p(**kw):
+    d = dict(STN_DEFAULTS)
+    d.update(kw)
+    return np.array([d[k] for k in O.PARAMS[O.STN]])
+
+
+def test_stn_uncoupled_closed_form():
+    # With w_ss = w_gs = w_sg = w_gg = 0, Eqs. 1-2 become linear:
+    # tau x' = -x + Z(const); RK4 gives x_n = x* + (x0 - x*) T4(-h/tau)^n exactly.
+    p = stn_p(w_ss=0, w_gs=0, w_sg=0, w_gg=0)
+    h, n = 0.01, 300
+    x0 = np.array([[0.9], [0.1]])
+    x = O.rk4(O.STN, x0, p, h, n)
+    xs = expit(STN_DEFAULTS["a_s"] * (STN_DEFAULTS["I"] - STN_DEFAULTS["theta_s"]))
+    ys = expit(STN_DEFAULTS["a_g"] * (0 - STN_DEFAULTS["theta_g"]))
+    T = lambda z: 1 + z + z * z / 2 + z ** 3 / 6 + z ** 4 / 24
+    assert x[0, 0] == pytest.approx(xs + (0.9 - xs) * T(-h / STN_DEFAULTS["tau_s"]) ** n, abs=1e-13)
+    assert x[1, 0] == pytest.approx(ys + (0.1 - ys) * T(-h / STN_DEFAULTS["tau_g"]) ** n, abs=1e-13)
+
+
+def test_stn_time_constants_scale_time():
+    # tau multiplies the whole left side (Eqs. 1-2): doubling tau_s, tau_g and h gives the same
+    # RK4 iterates (exact in real arithmetic; fp64 rounding only).
+    rng = np.random.default_rng(30)
+    x0 = rng.uniform(0, 1, (2, 20))
+    a = O.rk4(O.STN, x0, stn_p(w_ss=7.8), 0.01, 200)
+    b = O.rk4(O.STN, x0, stn_p(w_ss=7.8, tau_s=2.0, tau_g=5.54), 0.02, 200)
+    np.testing.assert_allclose(a, b, atol=1e-12)
+
+
+def test_stn_argument_signs_via_step_sigmoid():
+    # With a very steep sigmoid, Z_s(u) -> H(u - theta_s) and Z_g(u) -> H(u - theta_g), so
+    # tau x' + x tells which side of threshold w_ss x - w_gs y + I (excitatory STN, inhibitory GPe,
+    # PAPER.md:40) and -w_gg y + w_sg x fall.
+    p = stn_p(w_ss=2.0, w_gs=3.0, w_sg=4.0, w_gg=5.0, I=1.0, a_s=1e4, theta_s=1.5, a_g=1e4, theta_g=0.5,
+              tau_s=1.0, tau_g=1.0)
+    def z(x, y):
+        d = O.rhs(O.STN, [x, y], p)
+        return d[0] + x, d[1] + y
+    # u_s = 2x - 3y + 1 ; u_g = 4x - 5y
+    zs, zg = z(0.5, 0.1)    # u_s = 1.7 > 1.5 ; u_g = 1.5 > 0.5
+    assert zs == pytest.approx(1.0) and zg == pytest.approx(1.0)
+    zs, zg = z(0.5, 0.2)    # u_s = 1.4 < 1.5 ; u_g = 1.0 > 0.5
+    assert zs == pytest.approx(0.0, abs=1e-12) and zg == pytest.approx(1.0)
+    zs, zg = z(0.2, 0.1)    # u_s = 1.1 < 1.5 ; u_g = 0.3 < 0.5
+    assert zs == pytest.approx(0.0, abs=1e-12) and zg == pytest.approx(0.0, abs=1e-12)
+
+
+@pytest.mark.parametrize("w_ss", [0.0, 4.9, 7.8, 11.0])
+def test_stn_forward_invariance_of_unit_square(w_ss):
+    # activity is in (0,1) and Z in (0,1) makes (0,1)^2 forward-invariant.
+    rng = np.random.default_rng(31)
+    x = O.rk4(O.STN, rng.uniform(0, 1, (2, 500)), stn_p(w_ss=w_ss), 0.01, 1000)
+    assert np.all((x > 0) & (x < 1))
+
+
+def test_stn_backward_particles_leave():
+    # backward particles "move very quickly out of the bounds of the system".
+    rng = np.random.default_rng(32)
+    x = O.rk4(O.STN, rng.uniform(0, 1, (2, 500)), stn_p(), -0.01, 1000)
+    out = np.any((x < 0) | (x > 1), axis=0)
+    assert out.mean() > 0.95
