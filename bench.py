@@ -1,0 +1,371 @@
+"""Bench of the Fireflies hot path on B200 (contract: see DESIGN.md "Measurement").
+
+One bench "step" = one frame of the paper's main loop: zero the density image, then
+ONE fused launch that advances every particle S RK4 steps in registers and bins it into the image
+(ff_step). N=1 default workload = BASELINE.json configs[1]: Lorenz (sigma 10, r 28, beta 8/3),
+2^22 forward + 2^22 backward particles from the Fig. 3A box, dt 0.01, 3-D
+perspective density image 1024 x 1024 x 2 channels, S = 100 steps per frame.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config lorenz3d|stn|hh|sweep|lorenz1b]
+                  [--S steps_per_frame] [--impl ours|reference]
+
+Under torchrun (N > 1) every rank runs the same per-rank workload on its shard (weak scaling) and
+the per-frame image is summed with an NCCL all-reduce (the path's one exchange step, SURVEY.md
+8(e)); the time is the max over ranks. --impl reference times the CPU oracle (the tier's reference
+arm) on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-steps/s per B200 and per box (Lorenz RK4, 15-D neuron); % FP32 peak"
+N_SM = 148
+FMA_LANES = 128   # FP32 lanes per SM (FFMA2 does not raise it: profiles/r01_ubench_pipes.txt)
+XU_LANES = 16     # MUFU results per clock per SM (same microbenchmark)
+
+# Algorithmic work per particle-step: FP32 FMA-pipe lane-ops of the plain
+# formulation with a*b+c contracted (Lorenz: 4 RHS x 6 + 3 dims x 7 RK4 combination = 45), MUFU ops
+# (exp2 / rcp per evaluation x 4), and HBM bytes per launch-particle (state in + out).
+WORKLOADS = {
+    "lorenz3d": dict(system="lorenz", groups=[(1 << 22, 1, 0, 2), (1 << 22, -1, 1, 3)], params={"r": 28.0},
+                     box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj="lorenz_camera", W=1024, H=1024, C=2,
+                     S=100, dt=0.01, fma_ops=45, mufu_ops=0, bound="alu",
+                     desc="Lorenz r=28, 4M fwd + 4M bwd, 3-D perspective image 1024x1024x2"),
+    "stn": dict(system="stn_gpe", groups=[(5000, 1, 0, 1), (5000, -1, 1, 11)], params={},
+                box=([0.0, 0.0], [1.0, 1.0]), proj=([0, 1], [0.0, 1.0, 0.0, 1.0]), W=512, H=512, C=2,
+                S=1000, dt=0.01, fma_ops=None, mufu_ops=16, bound="xu",
+                desc="STN-GPe 5k fwd + 5k bwd, 1000 steps, 2-D image 512x512x2 (configs[0])"),
+    "hh": dict(system="hh_ring3", groups=[(1 << 20, 1, 0, 4)], params={},
+               box=([-20.0, 0, 0, 0, 0] * 3, [100.0, 1, 1, 1, 1] * 3), proj=([0, 5], [-20.0, 120.0, -20.0, 120.0]),
+               W=1024, H=1024, C=1, S=100, dt=0.01, fma_ops=None, mufu_ops=132, bound="xu",
+               desc="HH ring N=3 (15-D), 1M particles, 2-D (V1,V2) image 1024x1024 (configs[2])"),
+    "sweep": dict(system="lorenz", groups=[(1 << 24, 1, 0, 5)], params={}, sweep=("r", 0.0, 200.0, 0, 5),
+                  box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj=([3, 1], [0.0, 200.0, -160.0, 160.0]),
+                  W=2048, H=1024, C=1, S=100, dt=0.01, fma_ops=45, mufu_ops=0, bound="alu",
+                  desc="Lorenz r swept in [0,200), 16M particles, (r, y) image 2048x1024 (configs[3])"),
+    "lorenz1b": dict(system="lorenz", groups=[(1 << 30, 1, 0, 6)], params={"r": 28.0}, strong=True,
+                     box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj="lorenz_camera", W=1024, H=1024, C=1,
+                     S=100, dt=0.01, fma_ops=45, mufu_ops=0, bound="alu",
+                     desc="Lorenz 1B particles sharded over the GPUs (configs[4])"),
+}
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop_ev, self.max_mhz = [], set(), threading.Event(), None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x40: "sw_thermal_slowdown",
+                 0x80: "hw_thermal_slowdown", 0x100: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in names.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_ev.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_system(name):
+    from paper_1505_00344_b200 import systems
+    return {"lorenz": systems.lorenz, "stn_gpe": systems.stn_gpe, "hh_ring3": lambda: systems.hh_ring(3)}[name]()
+
+
+def projection(w):
+    from paper_1505_00344_b200 import views
+    if w["proj"] == "lorenz_camera":
+        return [0, 1, 2], views.lorenz_camera()
+    return w["proj"]
+
+
+def run_ours(args, w, rank, world, device):
+    import torch
+    import paper_1505_00344_b200 as FF
+    S = args.S or w["S"]
+    strong = w.get("strong", False)
+    # weak scaling: every rank holds the full per-rank workload (global groups = world x per-rank)
+    gsizes = [n if strong else n * world for (n, _, _, _) in w["groups"]]
+    ctx = FF.Context(make_system(w["system"]), gsizes, rank=rank, world=world)
+    for k, v in w["params"].items():
+        ctx.set_param(k, v)
+    if args.ppt or args.tpb:
+        ctx.set_launch(args.ppt, args.tpb)
+    lo, hi = w["box"]
+    gids = []
+    for (n, d, colour, seed), ng in zip(w["groups"], gsizes):
+        gids.append(ctx.init_group(lo, hi, ng, d, colour, seed))
+    if "sweep" in w:
+        name, a, b, mode, seed = w["sweep"]
+        for g in gids:
+            ctx.sweep_param(g, name, a, b, mode, seed)
+    axes, view = projection(w)
+    img = ctx.project(axes, view, w["W"], w["H"], w["C"])
+    n_local = sum(ctx.group_info(g)[1] for g in gids)
+    stream = ctx.stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)   # > 126 MB L2
+    dist = world > 1
+
+    def frame():
+        img.zero_()
+        ctx.step(S, w["dt"])
+        if dist:
+            torch.distributed.all_reduce(img)
+
+    for _ in range(args.warmup):
+        frame()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    launches0 = ctx.launch_count()
+    if dist:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(device.index) as clk:
+        t_wall = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()                       # L2 flush between timed iterations (not timed)
+            ev[i][0].record(stream)
+            img.zero_()
+            ev[i][1].record(stream)
+            ctx.step(S, w["dt"])
+            ev[i][2].record(stream)
+            if dist:
+                torch.distributed.all_reduce(img)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    if dist:
+        torch.distributed.barrier()
+    launches = ctx.launch_count() - launches0
+    frame_ms = np.array([ev[i][0].elapsed_time(ev[i][2]) for i in range(args.steps)])
+    kern_ms = np.array([ev[i][1].elapsed_time(ev[i][2]) for i in range(args.steps)])
+    t_total = float(frame_ms.sum())
+    if dist:
+        t = torch.tensor([t_total, float(kern_ms.mean())], dtype=torch.float64, device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_total, kern_mean = float(t[0]), float(t[1])
+        nt = torch.tensor([n_local], dtype=torch.float64, device=device)
+        torch.distributed.all_reduce(nt)
+        n_total = int(nt.item())
+    else:
+        kern_mean = float(kern_ms.mean())
+        n_total = n_local
+
+    # end-to-end through the C ABI with host buffers: pinned host state in, image out, every frame
+    e2e = None
+    if not dist and not args.no_e2e:
+        host_in = [torch.from_numpy(ctx.read_state(g)).pin_memory() for g in gids]
+        host_img = torch.empty(tuple(img.shape), dtype=torch.int32).pin_memory()
+        h2d = sum(t.numel() * 4 for t in host_in)
+        d2h = host_img.numel() * 4
+        from paper_1505_00344_b200 import fireflies as F
+
+        def e2e_frame():
+            for g, t in zip(gids, host_in):
+                F.check(F.lib().ff_write_state(ctx.ctx, g, 0, t.shape[1], F.C.c_void_p(t.data_ptr())))
+            img.zero_()
+            ctx.step(S, w["dt"])
+            F.ff_read_image_into(ctx.ctx, host_img.data_ptr())
+
+        for _ in range(2):
+            e2e_frame()
+        ke = max(3, min(args.steps, 20))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ke):
+            e2e_frame()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / ke
+        e2e = {"value": n_local * S / (ms * 1e-3), "unit": "particle-steps/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ms}
+    im_sum = int(img.sum().item())
+    ctx.close()
+    return dict(S=S, n_total=n_total, n_local=n_local, t_total_ms=t_total, kern_ms=kern_mean,
+                frame_ms=frame_ms, launches=launches, clocks=clk.summary(), e2e=e2e, image_sum=im_sum,
+                t_wall=t_wall)
+
+
+def cpu_oracle_sample(w, n_sample, S):
+    """Time the oracle (as it stands) on n_sample particles of the workload x S steps + binning."""
+    import oracle as O
+    model = {"lorenz": O.LORENZ, "stn_gpe": O.STN, "hh_ring3": O.HH}[w["system"]]
+    sysdef = make_system(w["system"])
+    pvals = {p[0]: p[1] for p in sysdef.params}
+    pvals.update(w["params"])
+    if model == O.HH:
+        names = O.hh_param_names(3)
+    else:
+        names = O.PARAMS[model]
+    p = np.array([pvals[k] for k in names], np.float32)
+    lo, hi = w["box"]
+    x = O.ic_uniform(lo, hi, w["groups"][0][3], 0, n_sample)
+    sweep_idx, sv = -1, None
+    if "sweep" in w:
+        name, a, b, mode, seed = w["sweep"]
+        sweep_idx = names.index(name)
+        sv = O.sweep_values(a, b, mode, seed, 0, n_sample, w["groups"][0][0])
+    axes, view = projection(w)
+    t0 = time.perf_counter()
+    x = O.rk4(model, x, p, np.float32(w["dt"]), S, sweep_idx, sv)
+    O.histogram(x, axes, view, w["W"], w["H"], w["C"], 0, sweep_vals=sv)
+    dt = time.perf_counter() - t0
+    threads = int(os.environ.get("OMP_NUM_THREADS", 0)) or len(os.sched_getaffinity(0))
+    return n_sample * S / dt, dt, threads
+
+
+def reference_sample_size(w, S):
+    # bounded sample: ~1e8 particle-steps of Lorenz-size work (HH ~30x costlier per step)
+    per = {"lorenz": 1 << 22, "stn_gpe": 1 << 21, "hh_ring3": 1 << 17}[w["system"]]
+    return max(1024, int(per * 100 / S))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="lorenz3d", choices=sorted(WORKLOADS))
+    ap.add_argument("--S", type=int, default=0, help="RK4 steps per frame (default per config)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ppt", type=int, default=0)
+    ap.add_argument("--tpb", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    w = WORKLOADS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    S = args.S or w["S"]
+    config = {"workload": args.config, "description": w["desc"], "steps_per_frame": S, "dt": w["dt"],
+              "particles_per_gpu": (sum(g[0] for g in w["groups"]) // (world if w.get("strong") else 1)),
+              "image": [w["C"], w["H"], w["W"]], "l2": "flushed between timed frames (256 MiB memset)",
+              "parallelism": f"particles sharded over {world} GPU(s), NCCL image all-reduce per frame"
+              if world > 1 else "1 GPU"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        n = reference_sample_size(w, S)
+        vals, threads = [], 1
+        for _ in range(args.warmup if args.warmup < 3 else 1):
+            cpu_oracle_sample(w, max(256, n // 16), S)
+        for _ in range(args.steps if args.steps <= 5 else 5):
+            v, dt, threads = cpu_oracle_sample(w, n, S)
+            vals.append(v)
+        v = float(np.median(vals))
+        sample = f"{n} particles of the workload x {S} RK4 steps + binning per step (oracle, FP32, OpenMP)"
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "particle-steps/s", "n_gpus": args.gpus,
+                "steps": len(vals), "warmup": args.warmup, "ms_per_step": n * S / v * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
+                "cpu_baseline": {"value": v, "unit": "particle-steps/s", "cores": threads, "kind": "oracle",
+                                 "sample": sample},
+                "e2e": {"value": v, "unit": "particle-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    r = run_ours(args, w, rank, world, device)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    if rank != 0:
+        return
+    peaks = load_peaks()
+    psteps = r["n_total"] * r["S"] * args.steps
+    value = psteps / (r["t_total_ms"] * 1e-3)
+    clocks = r["clocks"]
+    f_max = (peaks.get("sm_max_mhz") or clocks.get("sm_max_mhz") or 1965.0) * 1e6
+    kern_s = r["kern_ms"] * 1e-3
+    per_launch = r["n_local"] * r["S"]
+    if w["bound"] == "alu":
+        achieved = per_launch * w["fma_ops"] / kern_s
+        peak = N_SM * FMA_LANES * f_max
+        roof = {"bound": "alu", "unit": "Tops/s (FP32 FMA-pipe lane-ops, FMA = 1 op)",
+                "achieved": achieved / 1e12, "peak": peak / 1e12, "frac": achieved / peak,
+                "peak_source": f"148 SM x 128 FP32 lanes x {f_max / 1e6:.0f} MHz (MEASURED_PEAKS sm_max_mhz; "
+                               "B200_PROFILING.md unit counts; FFMA2 measured at 128 lanes/clk)",
+                "alg_ops_per_particle_step": w["fma_ops"]}
+    else:
+        achieved = per_launch * w["mufu_ops"] / kern_s
+        peak = N_SM * XU_LANES * f_max
+        roof = {"bound": "alu", "pipe": "xu", "unit": "Tops/s (MUFU ex2/rcp results)",
+                "achieved": achieved / 1e12, "peak": peak / 1e12, "frac": achieved / peak,
+                "peak_source": f"148 SM x 16 MUFU/clk x {f_max / 1e6:.0f} MHz (profiles/r01_ubench_pipes.txt)",
+                "alg_ops_per_particle_step": w["mufu_ops"]}
+    roof["traffic"] = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        t = json.load(open(prof)).get(f"{args.config}_S{r['S']}")
+        if t:
+            roof["traffic"] = t
+    if clocks.get("sm_mhz"):
+        roof["frac_at_measured_clock"] = roof["frac"] * f_max / (clocks["sm_mhz"] * 1e6)
+    line = {"metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["t_total_ms"] / args.steps, "higher_is_better": True,
+            "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (Philox ICs from the paper's IC boxes)", "config": config,
+            "pct_fp32_peak": 100 * roof["frac"] if w["bound"] == "alu" else None,
+            "roofline": roof, "clocks": clocks, "gpu_launches": r["launches"], "e2e": r["e2e"],
+            "kernel_ms_mean": r["kern_ms"], "frame_ms_p10_p50_p90": [float(np.percentile(r["frame_ms"], q))
+                                                                     for q in (10, 50, 90)],
+            "image_sum_last_frame": r["image_sum"], "wall_s_timed_region": r["t_wall"]}
+    if world == 1 and not args.no_cpu_baseline:
+        n = reference_sample_size(w, r["S"])
+        v, dt, threads = cpu_oracle_sample(w, n, r["S"])
+        line["cpu_baseline"] = {"value": v, "unit": "particle-steps/s", "cores": threads, "kind": "oracle",
+                                "sample": f"{n} particles x {r['S']} RK4 steps + binning ({dt:.1f} s)"}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

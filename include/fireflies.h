@@ -1,0 +1,211 @@
+/* fireflies.h -- C ABI of the B200-native Fireflies hot path (arXiv:1505.00344).
+ *
+ * The library integrates many independent trajectories ("particles") of a user-defined
+ * N-dimensional ODE with fixed-step classical RK4, each particle with its
+ * own initial condition, its own time direction and optionally its own
+ * value of one swept parameter, and bins the particles, projected onto 2 or 3
+ * chosen axes, into a density image.
+ *
+ * Conventions for every call:
+ *   - Every function returns ff_status; nothing is thrown across the ABI. On failure the
+ *     message is available from ff_last_error() (thread-local, valid until the next call on
+ *     the same thread). Failed calls leave the context unchanged unless stated otherwise.
+ *   - "device pointer" = CUDA global-memory pointer valid in the current device's primary
+ *     context (e.g. torch.Tensor.data_ptr() of a CUDA tensor). "host pointer" = CPU memory.
+ *   - Device memory for particle state and images is CALLER-OWNED. The context stores non-owning
+ *     pointers and never frees them; ff_destroy frees only what the library allocated
+ *     (compiled modules, tables).
+ *   - Launches are asynchronous on the stream set with ff_set_stream (default: the legacy
+ *     default stream). Parameter values are captured by value at launch, so ff_set_param takes
+ *     effect at the next launch and never needs a device sync.
+ *   - A context is NOT thread-safe; use one per host thread / device.
+ *   - All floating-point state is FP32 ("single-precision floating point values",
+ *     PAPER.md:225).
+ */
+#ifndef FIREFLIES_H
+#define FIREFLIES_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FF_ABI_VERSION 1
+#define FF_MAX_DIM 64      /* state variables per system */
+#define FF_MAX_PARAMS 128  /* parameters per system */
+#define FF_MAX_GROUPS 16   /* particle groups per context */
+#define FF_TILE 512        /* group slot ranges are padded to a multiple of this */
+
+typedef enum {
+  FF_OK = 0,
+  FF_ERR_INVALID_ARG = 1,    /* bad pointer / size / range / enum value */
+  FF_ERR_PARSE = 2,          /* expression syntax error, unknown function, wrong arity */
+  FF_ERR_UNKNOWN_SYMBOL = 3, /* identifier that is neither a state variable nor a parameter */
+  FF_ERR_RANGE = 4,          /* parameter value outside [min, max] (rejected, not clamped) */
+  FF_ERR_COMPILE = 5,        /* NVRTC failure (message holds the log) */
+  FF_ERR_CUDA = 6,           /* CUDA runtime / launch failure (message holds the CUDA error) */
+  FF_ERR_OOM = 7,            /* host allocation failure */
+  FF_ERR_STATE = 8           /* call not valid in the current context state */
+} ff_status;
+
+typedef struct ff_ctx ff_ctx; /* opaque */
+
+/* System definition (State Variables with right-hand sides, Parameters with a
+ * default and a range of allowable values). All strings are NUL-terminated ASCII, copied by the
+ * library; the struct may be freed after the call.
+ *   dim            number of state variables, 1..FF_MAX_DIM
+ *   var_names[i]   identifier of state variable i ([A-Za-z_][A-Za-z0-9_]*)
+ *   rhs[i]         expression for d(var_i)/dt. Grammar (no conditionals):
+ *                    expr := term (("+"|"-") term)* ; term := factor (("*"|"/") factor)*
+ *                    factor := "-" factor | power ; power := atom ("^" factor)?
+ *                    atom := number | ident | ident "(" expr ("," expr)* ")" | "(" expr ")"
+ *                  functions: exp log sin cos tan tanh sqrt abs sigmoid (1 arg), pow min max vtrap
+ *                  (2 args); sigmoid(u) = 1/(1+exp(-u)); vtrap(x,y) = x/(exp(x/y)-1) with its
+ *                  removable singularity at x = 0 handled (reading R10).
+ *                  Constants: pi, e. Names may not shadow each other, pi, e or a function.
+ *   n_params       0..FF_MAX_PARAMS
+ *   param_names[k], param_default[k]; param_min / param_max may be NULL (unbounded), else
+ *                  min[k] <= default[k] <= max[k] is required. */
+typedef struct {
+  int dim;
+  const char* const* var_names;
+  const char* const* rhs;
+  int n_params;
+  const char* const* param_names;
+  const float* param_default;
+  const float* param_min;
+  const float* param_max;
+} ff_system;
+
+/* ---------------------------------------------------------------- library / front end */
+
+/* Message of the last failed call on this thread ("" if none). Never NULL. */
+const char* ff_last_error(void);
+
+/* FF_ABI_VERSION of the loaded library. */
+int ff_abi_version(void);
+
+/* Front end only (no device needed; "kernel source ... generated automatically"):
+ * parse, validate and emit the CUDA C source of the system's kernels. sweep_param = index of the
+ * parameter that is per-particle in this variant, or -1. Writes at most cap bytes (NUL-terminated)
+ * to buf; *len (if non-NULL) receives the full length excluding the NUL. buf may be NULL to query.
+ * Errors: FF_ERR_INVALID_ARG, FF_ERR_PARSE, FF_ERR_UNKNOWN_SYMBOL. */
+ff_status ff_emit_source(const ff_system* sys, int sweep_param, char* buf, size_t cap, size_t* len);
+
+/* Front end + NVRTC (no device needed): compile the emitted source to an sm_100a CUBIN.
+ * Same buffer protocol as ff_emit_source. Errors as ff_emit_source, plus FF_ERR_COMPILE. */
+ff_status ff_compile_cubin(const ff_system* sys, int sweep_param, void* buf, size_t cap, size_t* len);
+
+/* ---------------------------------------------------------------- context */
+
+/* Parse + validate the system, compile its kernels (NVRTC, sm_100a CUBIN) and load them on
+ * `device` (which must be the calling thread's current CUDA device). *out receives the context.
+ * Errors: ff_emit_source's, FF_ERR_COMPILE, FF_ERR_CUDA (no device, module load failure). */
+ff_status ff_create(const ff_system* sys, int device, ff_ctx** out);
+
+/* Free the context and the library-owned resources. Does not free caller memory. NULL is OK. */
+ff_status ff_destroy(ff_ctx* ctx);
+
+/* Stream for every subsequent launch/copy (a cudaStream_t; NULL = legacy default stream). */
+ff_status ff_set_stream(ff_ctx* ctx, void* cuda_stream);
+
+/* Multi-GPU sharding: this process holds, of every group created afterwards,
+ * the contiguous index range [floor(n*rank/world), floor(n*(rank+1)/world)). Particle i keeps
+ * its group-global index, so initial conditions and swept values do not depend on world.
+ * Must be called before the first ff_init_group. Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE. */
+ff_status ff_set_shard(ff_ctx* ctx, int rank, int world);
+
+/* Bind caller-owned particle state: device pointer to float[dim][pitch] (SoA: component d of
+ * slot j at state[d*pitch + j]), 16-byte aligned, pitch a multiple of FF_TILE, capacity <= pitch
+ * slots usable. Must be called before the first ff_init_group (rebinding clears the groups).
+ * Errors: FF_ERR_INVALID_ARG (NULL, misaligned, pitch/capacity). */
+ff_status ff_bind_state(ff_ctx* ctx, float* dev_state, int64_t pitch, int64_t capacity);
+
+/* Query the minimum number of slots a group of n_global particles needs on this shard
+ * (its local count rounded up to FF_TILE). */
+ff_status ff_group_slots(ff_ctx* ctx, int64_t n_global, int64_t* slots);
+
+/* Create a particle group (count, direction, initial-condition cube) and launch
+ * its initial-condition kernel (async). ic_lo/ic_hi: HOST arrays of dim floats, the half-open
+ * box [lo, hi) per state variable (lo < hi, finite). n_global >= 1 particles in total over all
+ * shards; direction +1 (forward in time) or -1 (backward); colour = image channel this group is
+ * counted in (>= 0); seed keys the group's Philox stream (use distinct seeds for distinct groups).
+ * The group occupies the next free tile-aligned slot range; padding slots are set to NaN and are
+ * never binned. *group_id (may be NULL) receives the group's index.
+ * Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE (no state bound, too many groups, capacity
+ * exceeded), FF_ERR_CUDA. */
+ff_status ff_init_group(ff_ctx* ctx, const float* ic_lo, const float* ic_hi, int64_t n_global,
+                        int direction, int colour, uint64_t seed, int* group_id);
+
+/* Slot layout of a group on this shard: first slot, local particle count, and the group-global
+ * index of its first local particle. Any out pointer may be NULL. */
+ff_status ff_group_info(ff_ctx* ctx, int group_id, int64_t* slot_begin, int64_t* n_local,
+                        int64_t* first_global);
+
+/* Set a parameter by name ("updates the location in GPU memory where the
+ * corresponding parameter value is stored"); the next launch uses it.
+ * Errors: FF_ERR_UNKNOWN_SYMBOL, FF_ERR_RANGE (outside [min, max]; value is not clamped),
+ * FF_ERR_INVALID_ARG (non-finite). */
+ff_status ff_set_param(ff_ctx* ctx, const char* name, float value);
+ff_status ff_get_param(ff_ctx* ctx, const char* name, float* value);
+
+/* Make parameter `name` a per-particle value for group `group_id` (the lifted parameter of
+ * a state variable with zero derivative; here it is never integrated, so it is
+ * bit-unchanged by construction). mode 0: Philox-uniform in [lo, hi) keyed by `seed`;
+ * mode 1: linspace lo + (hi - lo) * (i + 0.5) / n_global. At most one parameter per context may
+ * be swept (all sweeping groups must name the same one); groups without a sweep use the
+ * parameter's current value. The value is recomputed from the particle index in every launch
+ * (0 bytes of state). It is addressable as axis index `dim` in ff_project.
+ * Errors: FF_ERR_UNKNOWN_SYMBOL, FF_ERR_INVALID_ARG (lo >= hi, mode, group), FF_ERR_STATE
+ * (another parameter already swept), FF_ERR_COMPILE (variant compile). */
+ff_status ff_sweep_param(ff_ctx* ctx, int group_id, const char* name, float lo, float hi, int mode,
+                         uint64_t seed);
+
+/* Bind the density image and bin the current state into it now (async).
+ * axes: HOST array of n_axes (2 or 3) indices into the extended state [0..dim-1 state vars,
+ *       dim = the swept parameter]; view: HOST array, 2-D: {lo_0, hi_0, lo_1, hi_1} (window, each
+ *       lo < hi), 3-D: row-major 4x4 view-projection matrix (rows 0, 1, 3 used).
+ * image: DEVICE pointer to uint32 [C][H][W] (caller-owned, caller zeroes it), 4-byte aligned.
+ * Binning rule (readings R17-R19): 2-D keeps lo <= v < hi on both axes,
+ *   ix = min(floor((v0 - lo0) * (W / (hi0 - lo0))), W - 1), likewise iy; 3-D computes
+ *   c_r = ((M[r][0] a + M[r][1] b) + M[r][2] c) + M[r][3], keeps c_w > 0,
+ *   px = (c_0 / c_w + 1) * (W / 2), keeps 0 <= px < W, likewise py. Each kept particle adds 1 to
+ *   image[colour(group)][iy][ix]; non-finite values and padding slots are dropped.
+ * Once bound, every ff_step adds one count per particle after its last step (fused). Pass
+ * image = NULL to unbind (no binning). Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE (colour of some
+ * group >= C), FF_ERR_CUDA. */
+ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view, int W, int H,
+                     int C, uint32_t* image);
+
+/* Advance every particle of every group by n_steps RK4 steps of signed size direction*dt
+ * (dt may be negative), then, if an image is bound, bin every particle once
+ * (fused). One kernel launch; async. n_steps >= 0 (0 = bin only).
+ * Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE (no groups), FF_ERR_CUDA. */
+ff_status ff_step(ff_ctx* ctx, int64_t n_steps, float dt);
+
+/* Kernel selection: particles per thread (1 or 2; 2 packs pairs into FFMA2) and threads per
+ * block (128, 256 or 512); 0 = library default. For tuning/benchmarks. */
+ff_status ff_set_launch(ff_ctx* ctx, int particles_per_thread, int threads_per_block);
+
+/* Copy particles [first, first+count) (group-local indices on this shard) of a group between the
+ * device state and a HOST SoA buffer float[dim][count]. Synchronous w.r.t. the host (the stream
+ * is synchronised). Errors: FF_ERR_INVALID_ARG (range), FF_ERR_CUDA. */
+ff_status ff_read_state(ff_ctx* ctx, int group_id, int64_t first, int64_t count, float* host_soa);
+ff_status ff_write_state(ff_ctx* ctx, int group_id, int64_t first, int64_t count,
+                         const float* host_soa);
+
+/* Copy the bound image to a HOST uint32 [C][H][W] buffer (synchronous). */
+ff_status ff_read_image(ff_ctx* ctx, uint32_t* host_image);
+
+/* Number of kernel launches this context has issued (for bench evidence). */
+ff_status ff_launch_count(ff_ctx* ctx, int64_t* count);
+
+/* Synchronise the bound stream; surfaces asynchronous kernel errors as FF_ERR_CUDA. */
+ff_status ff_sync(ff_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIREFLIES_H */

@@ -1,0 +1,49 @@
+// ff_args.h -- by-value launch argument blocks of the Fireflies kernels.
+//
+// Single source of truth for the layout: the host runtime (ff_runtime.cpp) includes this file,
+// and the build embeds it in front of ff_device.cuh in the NVRTC source. Kernel arguments live
+// in the constant bank, so parameters and per-group step sizes are read as FFMA operands
+// (parameters change "in GPU memory" without recompiling; here they are captured by
+// value at each launch).
+#ifndef FF_ARGS_H
+#define FF_ARGS_H
+
+typedef unsigned long long ff_u64;
+typedef long long ff_i64;
+typedef unsigned int ff_u32;
+
+#define FF_MAX_GROUPS_ 16
+#ifndef FF_NP_ALLOC
+#define FF_NP_ALLOC 128  /* host side: FF_MAX_PARAMS; device side: the system's count */
+#endif
+
+struct FFGroup {
+  ff_i64 slot_begin;    // first slot of the group (multiple of FF_TILE)
+  ff_i64 slot_end;      // padded end (multiple of FF_TILE)
+  ff_i64 n_local;       // real particles in [slot_begin, slot_begin + n_local)
+  ff_i64 first_global;  // group-global index of the first local particle
+  ff_i64 n_global;      // particles in the whole group (all shards)
+  ff_u64 sweep_seed;
+  float h, h2, h3, h6;  // signed step direction*dt and h/2, h/3, h/6
+  float sw_lo, sw_hi, sw_top, sw_val;  // sweep range, largest float below hi, uniform value
+  int sweep_mode;       // -1: every particle uses sw_val; 0: Philox-uniform; 1: linspace
+  int colour;           // image channel
+};
+
+struct FFStepArgs {
+  float* state;         // [dim][pitch] SoA
+  ff_i64 pitch;
+  ff_i64 slots_total;   // end of the last group's slot range
+  ff_i64 n_steps;
+  ff_u32* image;        // bound image [C][H][W] or null
+  int proj;             // 0 none, 2 (2-D window) or 3 (4x4 view-projection)
+  int W, H, C;
+  int axes[3];
+  float view[16];
+  float s0, s1;         // 2-D scales W/(hi0-lo0), H/(hi1-lo1), computed by the host in float
+  int n_groups;
+  FFGroup g[FF_MAX_GROUPS_];
+  float p[FF_NP_ALLOC]; // parameter values (must stay the last member)
+};
+
+#endif

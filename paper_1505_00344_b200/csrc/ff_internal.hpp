@@ -1,0 +1,63 @@
+// ff_internal.hpp -- shared declarations of the host side of libfireflies (front end + runtime).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fireflies.h"
+
+namespace ff {
+
+// Error carried to the ABI boundary, where it becomes an ff_status + ff_last_error() message.
+struct Error : std::runtime_error {
+  ff_status status;
+  Error(ff_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+// ---------------------------------------------------------------- expression AST
+enum class Op {
+  Num,     // literal (value)
+  Var,     // state variable (index)
+  Param,   // parameter (index)
+  Neg,     // -a
+  Add, Sub, Mul, Div, Pow,
+  Call     // function (name) with args
+};
+
+struct Node {
+  Op op;
+  double value = 0.0;
+  int index = -1;
+  std::string name;                  // function name for Call
+  std::vector<std::shared_ptr<Node>> args;
+  int pos = 0;                       // source position (for messages)
+};
+using NodeP = std::shared_ptr<Node>;
+
+// Validated system: names, parsed right-hand sides, parameter table.
+struct System {
+  int dim = 0;
+  std::vector<std::string> var_names;
+  std::vector<std::string> rhs_text;
+  std::vector<NodeP> rhs;
+  std::vector<std::string> param_names;
+  std::vector<float> param_default, param_min, param_max;
+};
+
+// Parse + validate an ff_system (throws Error).
+System parse_system(const ff_system* sys);
+
+// Emit the complete NVRTC source (generated prefix + device template) for the system with
+// parameter `sweep_param` (or -1) per-particle.
+std::string emit_source(const System& s, int sweep_param);
+
+// NVRTC: source -> sm_100a CUBIN (throws Error(FF_ERR_COMPILE) with the log).
+std::vector<char> compile_cubin(const std::string& source, const std::string& name);
+
+// The embedded device template text (ff_device.cuh), generated at build time.
+extern const char* const kDeviceTemplate;
+
+}  // namespace ff

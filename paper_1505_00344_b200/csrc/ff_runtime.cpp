@@ -1,0 +1,533 @@
+// ff_runtime.cpp -- the C ABI of libfireflies (include/fireflies.h): context, particle groups,
+// parameter table, sweep spec, projection binding and the launches.
+//
+// Design: caller-owned device memory (torch tensors), library-owned
+// compiled modules; every launch is async on the bound stream with a by-value argument block
+// (csrc/device/ff_args.h), so ff_set_param never touches the device.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstddef>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "device/ff_args.h"
+#include "ff_internal.hpp"
+
+static_assert(sizeof(FFGroup) == 88, "FFGroup layout");
+static_assert(offsetof(FFStepArgs, g) == 144, "FFStepArgs layout");
+static_assert(FF_MAX_GROUPS_ == FF_MAX_GROUPS, "group table size");
+
+namespace {
+
+thread_local std::string g_err;
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw ff::Error(FF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+struct Module {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t init = nullptr;
+  // step kernels by (ppt, tpb): index 0 p1t128, 1 p1t256, 2 p1t512, 3 p2t128, 4 p2t256
+  cudaKernel_t step[5] = {};
+  int occ[5] = {};
+};
+
+int step_index(int ppt, int tpb) {
+  if (ppt == 1) return tpb == 128 ? 0 : tpb == 256 ? 1 : tpb == 512 ? 2 : -1;
+  if (ppt == 2) return tpb == 128 ? 3 : tpb == 256 ? 4 : -1;
+  return -1;
+}
+const char* kStepNames[5] = {"ff_step_p1_t128", "ff_step_p1_t256", "ff_step_p1_t512", "ff_step_p2_t128",
+                             "ff_step_p2_t256"};
+const int kStepPPT[5] = {1, 1, 1, 2, 2};
+const int kStepTPB[5] = {128, 256, 512, 128, 256};
+
+struct GroupRec {
+  int64_t n_global = 0, first_global = 0, n_local = 0, slot_begin = 0, slot_end = 0;
+  int dir = 1, colour = 0;
+  uint64_t seed = 0;
+  std::vector<float> lo, hi;
+  int sweep_mode = -1;
+  float sw_lo = 0, sw_hi = 0;
+  uint64_t sw_seed = 0;
+};
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+}  // namespace
+
+struct ff_ctx {
+  ff::System sys;
+  std::vector<float> params;
+  int device = 0;
+  int nsm = 148;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  float* state = nullptr;
+  int64_t pitch = 0, capacity = 0, next_slot = 0;
+  std::vector<GroupRec> groups;
+  int sweep_param = -1;
+  std::map<int, Module> modules;  // by swept parameter index (-1 = none)
+  // projection binding
+  int proj = 0;
+  int axes[3] = {0, 0, 0};
+  float view[16] = {};
+  int W = 0, H = 0, C = 0;
+  uint32_t* image = nullptr;
+  float s0 = 0, s1 = 0;
+  int ppt = 0, tpb = 0;
+  int64_t launches = 0;
+
+  ~ff_ctx() {
+    for (auto& m : modules)
+      if (m.second.lib) cudaLibraryUnload(m.second.lib);
+  }
+
+  Module& module(int sweep) {
+    auto it = modules.find(sweep);
+    if (it != modules.end()) return it->second;
+    std::string src = ff::emit_source(sys, sweep);
+    std::vector<char> cubin = ff::compile_cubin(src, "fireflies_system.cu");
+    Module m;
+    ck(cudaLibraryLoadData(&m.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
+    ck(cudaLibraryGetKernel(&m.init, m.lib, "ff_init"), "cudaLibraryGetKernel(ff_init)");
+    for (int i = 0; i < 5; ++i) {
+      ck(cudaLibraryGetKernel(&m.step[i], m.lib, kStepNames[i]), "cudaLibraryGetKernel(ff_step)");
+      int occ = 0;
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m.step[i], kStepTPB[i], 0);
+      if (e != cudaSuccess) { cudaGetLastError(); occ = 1; }
+      m.occ[i] = occ > 0 ? occ : 1;
+    }
+    return modules.emplace(sweep, m).first->second;
+  }
+
+  int find_param(const char* name) const {
+    if (!name) throw ff::Error(FF_ERR_INVALID_ARG, "parameter name is NULL");
+    for (size_t k = 0; k < sys.param_names.size(); ++k)
+      if (sys.param_names[k] == name) return (int)k;
+    throw ff::Error(FF_ERR_UNKNOWN_SYMBOL, std::string("unknown parameter '") + name + "'");
+  }
+
+  const GroupRec& group(int gid) const {
+    if (gid < 0 || gid >= (int)groups.size()) throw ff::Error(FF_ERR_INVALID_ARG, "bad group id");
+    return groups[gid];
+  }
+
+  void default_launch(int& ppt_out, int& tpb_out) const {
+    ppt_out = ppt ? ppt : (sys.dim <= 8 ? 2 : 1);
+    tpb_out = tpb ? tpb : 256;
+  }
+
+  void launch_step(int64_t n_steps, float dt) {
+    if (groups.empty()) throw ff::Error(FF_ERR_STATE, "no particle groups");
+    if (!std::isfinite(dt)) throw ff::Error(FF_ERR_INVALID_ARG, "dt is not finite");
+    int p, t;
+    default_launch(p, t);
+    const int si = step_index(p, t);
+    Module& m = module(sweep_param);
+    FFStepArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.state = state;
+    a.pitch = pitch;
+    a.slots_total = next_slot;
+    a.n_steps = n_steps;
+    a.image = image;
+    a.proj = image ? proj : 0;
+    a.W = W;
+    a.H = H;
+    a.C = C;
+    for (int j = 0; j < 3; ++j) a.axes[j] = axes[j];
+    std::memcpy(a.view, view, sizeof view);
+    a.s0 = s0;
+    a.s1 = s1;
+    a.n_groups = (int)groups.size();
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      const GroupRec& G = groups[gi];
+      FFGroup& g = a.g[gi];
+      g.slot_begin = G.slot_begin;
+      g.slot_end = G.slot_end;
+      g.n_local = G.n_local;
+      g.first_global = G.first_global;
+      g.n_global = G.n_global;
+      const float h = (float)G.dir * dt;
+      g.h = h;
+      g.h2 = h * 0.5f;
+      g.h3 = h / 3.0f;
+      g.h6 = h / 6.0f;
+      g.colour = G.colour;
+      g.sweep_mode = (sweep_param >= 0) ? G.sweep_mode : -1;
+      g.sweep_seed = G.sw_seed;
+      g.sw_lo = G.sw_lo;
+      g.sw_hi = G.sw_hi;
+      g.sw_top = std::nextafter(G.sw_hi, -INFINITY);
+      g.sw_val = sweep_param >= 0 ? params[sweep_param] : 0.0f;
+    }
+    for (size_t k = 0; k < params.size(); ++k) a.p[k] = params[k];
+    const int64_t tile = (int64_t)p * t;
+    const int64_t ntiles = next_slot / tile;
+    if (ntiles == 0) return;
+    const int64_t resident = (int64_t)nsm * m.occ[si];
+    const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
+    void* args[] = {&a};
+    ck(cudaLaunchKernel((const void*)m.step[si], dim3(grid), dim3(t), args, 0, stream), "launch ff_step");
+    ++launches;
+  }
+};
+
+// ---------------------------------------------------------------- ABI helpers
+#define FF_TRY try {
+#define FF_CATCH                                                         \
+  }                                                                      \
+  catch (const ff::Error& e) {                                           \
+    g_err = e.what();                                                    \
+    return e.status;                                                     \
+  }                                                                      \
+  catch (const std::bad_alloc&) {                                        \
+    g_err = "out of host memory";                                        \
+    return FF_ERR_OOM;                                                   \
+  }                                                                      \
+  catch (const std::exception& e) {                                      \
+    g_err = e.what();                                                    \
+    return FF_ERR_INVALID_ARG;                                           \
+  }                                                                      \
+  return FF_OK;
+
+static void need(bool c, ff_status s, const char* msg) {
+  if (!c) throw ff::Error(s, msg);
+}
+
+static ff_status copy_out(const std::string& data, bool text, void* buf, size_t cap, size_t* len) {
+  if (len) *len = data.size();
+  if (buf && cap) {
+    if (text) {
+      size_t n = data.size() < cap - 1 ? data.size() : cap - 1;
+      std::memcpy(buf, data.data(), n);
+      static_cast<char*>(buf)[n] = '\0';
+    } else {
+      need(cap >= data.size(), FF_ERR_INVALID_ARG, "buffer too small");
+      std::memcpy(buf, data.data(), data.size());
+    }
+  }
+  return FF_OK;
+}
+
+extern "C" {
+
+const char* ff_last_error(void) { return g_err.c_str(); }
+
+int ff_abi_version(void) { return FF_ABI_VERSION; }
+
+ff_status ff_emit_source(const ff_system* sys, int sweep_param, char* buf, size_t cap, size_t* len) {
+  FF_TRY
+  ff::System s = ff::parse_system(sys);
+  std::string src = ff::emit_source(s, sweep_param);
+  return copy_out(src, true, buf, cap, len);
+  FF_CATCH
+}
+
+ff_status ff_compile_cubin(const ff_system* sys, int sweep_param, void* buf, size_t cap, size_t* len) {
+  FF_TRY
+  ff::System s = ff::parse_system(sys);
+  std::vector<char> c = ff::compile_cubin(ff::emit_source(s, sweep_param), "fireflies_system.cu");
+  return copy_out(std::string(c.begin(), c.end()), false, buf, cap, len);
+  FF_CATCH
+}
+
+ff_status ff_create(const ff_system* sys, int device, ff_ctx** out) {
+  FF_TRY
+  need(out != nullptr, FF_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  ff::System s = ff::parse_system(sys);
+  int ndev = 0;
+  ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  need(device >= 0 && device < ndev, FF_ERR_INVALID_ARG, "device index out of range");
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  ck(cudaFree(nullptr), "context init");
+  ff_ctx* c = new ff_ctx();
+  try {
+    c->sys = std::move(s);
+    c->params = c->sys.param_default;
+    c->device = device;
+    ck(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
+    c->module(-1);
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  *out = c;
+  FF_CATCH
+}
+
+ff_status ff_destroy(ff_ctx* ctx) {
+  FF_TRY
+  delete ctx;
+  FF_CATCH
+}
+
+ff_status ff_set_stream(ff_ctx* ctx, void* stream) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  ctx->stream = (cudaStream_t)stream;
+  FF_CATCH
+}
+
+ff_status ff_set_shard(ff_ctx* ctx, int rank, int world) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  need(world >= 1 && rank >= 0 && rank < world, FF_ERR_INVALID_ARG, "need 0 <= rank < world");
+  need(ctx->groups.empty(), FF_ERR_STATE, "ff_set_shard must precede ff_init_group");
+  ctx->rank = rank;
+  ctx->world = world;
+  FF_CATCH
+}
+
+ff_status ff_bind_state(ff_ctx* ctx, float* dev_state, int64_t pitch, int64_t capacity) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  need(dev_state != nullptr, FF_ERR_INVALID_ARG, "state pointer is NULL");
+  need(((uintptr_t)dev_state & 15) == 0, FF_ERR_INVALID_ARG, "state pointer must be 16-byte aligned");
+  need(pitch > 0 && pitch % FF_TILE == 0, FF_ERR_INVALID_ARG, "pitch must be a positive multiple of FF_TILE");
+  need(capacity >= 0 && capacity <= pitch, FF_ERR_INVALID_ARG, "need 0 <= capacity <= pitch");
+  ctx->state = dev_state;
+  ctx->pitch = pitch;
+  ctx->capacity = capacity;
+  ctx->next_slot = 0;
+  ctx->groups.clear();
+  FF_CATCH
+}
+
+static int64_t shard_begin(int64_t n, int r, int w) { return (int64_t)((__int128)n * r / w); }
+
+ff_status ff_group_slots(ff_ctx* ctx, int64_t n_global, int64_t* slots) {
+  FF_TRY
+  need(ctx && slots, FF_ERR_INVALID_ARG, "NULL argument");
+  need(n_global >= 1, FF_ERR_INVALID_ARG, "n_global must be >= 1");
+  int64_t nl = shard_begin(n_global, ctx->rank + 1, ctx->world) - shard_begin(n_global, ctx->rank, ctx->world);
+  *slots = round_up(nl, FF_TILE);
+  FF_CATCH
+}
+
+ff_status ff_init_group(ff_ctx* ctx, const float* ic_lo, const float* ic_hi, int64_t n_global, int direction,
+                        int colour, uint64_t seed, int* group_id) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  need(ic_lo && ic_hi, FF_ERR_INVALID_ARG, "ic_lo / ic_hi is NULL");
+  need(n_global >= 1, FF_ERR_INVALID_ARG, "n_global must be >= 1");
+  need(direction == 1 || direction == -1, FF_ERR_INVALID_ARG, "direction must be +1 or -1");
+  need(colour >= 0, FF_ERR_INVALID_ARG, "colour must be >= 0");
+  need(ctx->state != nullptr, FF_ERR_STATE, "no state bound (ff_bind_state)");
+  need((int)ctx->groups.size() < FF_MAX_GROUPS, FF_ERR_STATE, "too many groups");
+  const int dim = ctx->sys.dim;
+  GroupRec g;
+  for (int d = 0; d < dim; ++d) {
+    need(std::isfinite(ic_lo[d]) && std::isfinite(ic_hi[d]) && ic_lo[d] < ic_hi[d], FF_ERR_INVALID_ARG,
+         "initial-condition box needs finite lo < hi in every dimension");
+    g.lo.push_back(ic_lo[d]);
+    g.hi.push_back(ic_hi[d]);
+  }
+  g.n_global = n_global;
+  g.first_global = shard_begin(n_global, ctx->rank, ctx->world);
+  g.n_local = shard_begin(n_global, ctx->rank + 1, ctx->world) - g.first_global;
+  g.slot_begin = ctx->next_slot;
+  g.slot_end = g.slot_begin + round_up(g.n_local, FF_TILE);
+  need(g.slot_end <= ctx->capacity, FF_ERR_STATE, "state capacity exceeded");
+  g.dir = direction;
+  g.colour = colour;
+  g.seed = seed;
+  if (ctx->image && colour >= ctx->C) throw ff::Error(FF_ERR_STATE, "colour >= channels of the bound image");
+  Module& m = ctx->module(ctx->sweep_param);
+  if (g.slot_end > g.slot_begin) {
+    // FFInitArgs (ff_device.cuh): 7 x 8-byte fields, then lo[dim], hi[dim], top[dim] floats.
+    std::vector<unsigned char> buf(56 + 12 * (size_t)dim + 8, 0);
+    int64_t f[6] = {(int64_t)(uintptr_t)ctx->state, ctx->pitch, g.slot_begin, g.slot_end, g.n_local, g.first_global};
+    std::memcpy(buf.data(), f, 48);
+    std::memcpy(buf.data() + 48, &seed, 8);
+    float* fl = reinterpret_cast<float*>(buf.data() + 56);
+    for (int d = 0; d < dim; ++d) {
+      fl[d] = g.lo[d];
+      fl[dim + d] = g.hi[d];
+      fl[2 * dim + d] = std::nextafter(g.hi[d], -INFINITY);
+    }
+    void* args[] = {buf.data()};
+    const unsigned grid = (unsigned)((g.slot_end - g.slot_begin) / 256);
+    ck(cudaLaunchKernel((const void*)m.init, dim3(grid), dim3(256), args, 0, ctx->stream), "launch ff_init");
+    ++ctx->launches;
+  }
+  ctx->next_slot = g.slot_end;
+  ctx->groups.push_back(g);
+  if (group_id) *group_id = (int)ctx->groups.size() - 1;
+  FF_CATCH
+}
+
+ff_status ff_group_info(ff_ctx* ctx, int group_id, int64_t* slot_begin, int64_t* n_local, int64_t* first_global) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  const GroupRec& g = ctx->group(group_id);
+  if (slot_begin) *slot_begin = g.slot_begin;
+  if (n_local) *n_local = g.n_local;
+  if (first_global) *first_global = g.first_global;
+  FF_CATCH
+}
+
+ff_status ff_set_param(ff_ctx* ctx, const char* name, float value) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  const int k = ctx->find_param(name);
+  need(std::isfinite(value), FF_ERR_INVALID_ARG, "parameter value is not finite");
+  if (!(value >= ctx->sys.param_min[k] && value <= ctx->sys.param_max[k]))
+    throw ff::Error(FF_ERR_RANGE, std::string("value outside the allowed range of '") + name + "'");
+  ctx->params[k] = value;
+  FF_CATCH
+}
+
+ff_status ff_get_param(ff_ctx* ctx, const char* name, float* value) {
+  FF_TRY
+  need(ctx && value, FF_ERR_INVALID_ARG, "NULL argument");
+  *value = ctx->params[ctx->find_param(name)];
+  FF_CATCH
+}
+
+ff_status ff_sweep_param(ff_ctx* ctx, int group_id, const char* name, float lo, float hi, int mode, uint64_t seed) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  const int k = ctx->find_param(name);
+  ctx->group(group_id);
+  need(std::isfinite(lo) && std::isfinite(hi) && lo < hi, FF_ERR_INVALID_ARG, "sweep range needs finite lo < hi");
+  need(mode == 0 || mode == 1, FF_ERR_INVALID_ARG, "mode must be 0 (uniform) or 1 (linspace)");
+  need(ctx->sweep_param < 0 || ctx->sweep_param == k, FF_ERR_STATE, "another parameter is already swept");
+  ctx->module(k);  // compile the variant now so errors surface here
+  ctx->sweep_param = k;
+  GroupRec& g = ctx->groups[group_id];
+  g.sweep_mode = mode;
+  g.sw_lo = lo;
+  g.sw_hi = hi;
+  g.sw_seed = seed;
+  FF_CATCH
+}
+
+ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view, int W, int H, int C,
+                     uint32_t* image) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  if (!image) {
+    ctx->image = nullptr;
+    ctx->proj = 0;
+    return FF_OK;
+  }
+  need(axes && view, FF_ERR_INVALID_ARG, "axes / view is NULL");
+  need(n_axes == 2 || n_axes == 3, FF_ERR_INVALID_ARG, "n_axes must be 2 or 3");
+  need(W >= 1 && H >= 1 && C >= 1, FF_ERR_INVALID_ARG, "W, H, C must be >= 1");
+  need((uint64_t)W * H * C < 0xffffffffull, FF_ERR_INVALID_ARG, "image too large");
+  need(((uintptr_t)image & 3) == 0, FF_ERR_INVALID_ARG, "image must be 4-byte aligned");
+  for (int j = 0; j < n_axes; ++j) {
+    need(axes[j] >= 0 && axes[j] <= ctx->sys.dim, FF_ERR_INVALID_ARG, "axis index out of range");
+    need(axes[j] < ctx->sys.dim || ctx->sweep_param >= 0, FF_ERR_INVALID_ARG,
+         "axis index dim names the swept parameter, but none is swept");
+  }
+  for (const GroupRec& g : ctx->groups) need(g.colour < C, FF_ERR_STATE, "a group's colour is >= C");
+  float v[16] = {};
+  if (n_axes == 2) {
+    for (int j = 0; j < 4; ++j) need(std::isfinite(view[j]), FF_ERR_INVALID_ARG, "window is not finite");
+    need(view[0] < view[1] && view[2] < view[3], FF_ERR_INVALID_ARG, "window needs lo < hi");
+    std::memcpy(v, view, 4 * sizeof(float));
+    ctx->s0 = (float)W / (view[1] - view[0]);
+    ctx->s1 = (float)H / (view[3] - view[2]);
+  } else {
+    for (int j = 0; j < 16; ++j) need(std::isfinite(view[j]), FF_ERR_INVALID_ARG, "matrix is not finite");
+    std::memcpy(v, view, 16 * sizeof(float));
+  }
+  ctx->proj = n_axes;
+  for (int j = 0; j < 3; ++j) ctx->axes[j] = axes[j < n_axes ? j : 0];
+  std::memcpy(ctx->view, v, sizeof v);
+  ctx->W = W;
+  ctx->H = H;
+  ctx->C = C;
+  ctx->image = image;
+  if (!ctx->groups.empty()) ctx->launch_step(0, 0.0f);
+  FF_CATCH
+}
+
+ff_status ff_step(ff_ctx* ctx, int64_t n_steps, float dt) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  need(n_steps >= 0, FF_ERR_INVALID_ARG, "n_steps must be >= 0");
+  ctx->launch_step(n_steps, dt);
+  FF_CATCH
+}
+
+ff_status ff_set_launch(ff_ctx* ctx, int ppt, int tpb) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  need(ppt == 0 || ppt == 1 || ppt == 2, FF_ERR_INVALID_ARG, "particles per thread must be 0, 1 or 2");
+  need(tpb == 0 || tpb == 128 || tpb == 256 || tpb == 512, FF_ERR_INVALID_ARG, "threads per block must be 0/128/256/512");
+  int p = ppt ? ppt : (ctx->sys.dim <= 8 ? 2 : 1), t = tpb ? tpb : 256;
+  need(step_index(p, t) >= 0, FF_ERR_INVALID_ARG, "unsupported (ppt, tpb) combination");
+  ctx->ppt = ppt;
+  ctx->tpb = tpb;
+  FF_CATCH
+}
+
+static void state_copy(ff_ctx* ctx, int group_id, int64_t first, int64_t count, void* host, bool to_host) {
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  const GroupRec& g = ctx->group(group_id);
+  need(host || count == 0, FF_ERR_INVALID_ARG, "host buffer is NULL");
+  need(first >= 0 && count >= 0 && first + count <= g.n_local, FF_ERR_INVALID_ARG, "particle range out of bounds");
+  if (count == 0) return;
+  const size_t w = (size_t)count * sizeof(float);
+  float* dev = ctx->state + g.slot_begin + first;
+  if (to_host) {
+    ck(cudaMemcpy2DAsync(host, w, dev, (size_t)ctx->pitch * sizeof(float), w, ctx->sys.dim, cudaMemcpyDeviceToHost,
+                         ctx->stream), "cudaMemcpy2DAsync D2H");
+  } else {
+    ck(cudaMemcpy2DAsync(dev, (size_t)ctx->pitch * sizeof(float), host, w, w, ctx->sys.dim, cudaMemcpyHostToDevice,
+                         ctx->stream), "cudaMemcpy2DAsync H2D");
+  }
+  ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+}
+
+ff_status ff_read_state(ff_ctx* ctx, int group_id, int64_t first, int64_t count, float* host_soa) {
+  FF_TRY
+  state_copy(ctx, group_id, first, count, host_soa, true);
+  FF_CATCH
+}
+
+ff_status ff_write_state(ff_ctx* ctx, int group_id, int64_t first, int64_t count, const float* host_soa) {
+  FF_TRY
+  state_copy(ctx, group_id, first, count, const_cast<float*>(host_soa), false);
+  FF_CATCH
+}
+
+ff_status ff_read_image(ff_ctx* ctx, uint32_t* host_image) {
+  FF_TRY
+  need(ctx && host_image, FF_ERR_INVALID_ARG, "NULL argument");
+  need(ctx->image != nullptr, FF_ERR_STATE, "no image bound");
+  ck(cudaMemcpyAsync(host_image, ctx->image, (size_t)ctx->W * ctx->H * ctx->C * sizeof(uint32_t),
+                     cudaMemcpyDeviceToHost, ctx->stream), "cudaMemcpyAsync D2H image");
+  ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+  FF_CATCH
+}
+
+ff_status ff_launch_count(ff_ctx* ctx, int64_t* count) {
+  FF_TRY
+  need(ctx && count, FF_ERR_INVALID_ARG, "NULL argument");
+  *count = ctx->launches;
+  FF_CATCH
+}
+
+ff_status ff_sync(ff_ctx* ctx) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+  ck(cudaGetLastError(), "kernel error");
+  FF_CATCH
+}
+
+}  // extern "C"

@@ -1,0 +1,334 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical seeded inputs.
+
+Bars: initial conditions and swept values bit-exact; histograms bit-exact on
+identical coordinates; state within the scaled tolerance e <= 1e-5 (Tier A) over the horizons
+calibrated in SURVEY.md 8(c), statistical Tier B beyond them.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from parity import dim_scales, finite_agreement, oracle_group, scaled_error, tier_a
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1505_00344_b200 as FF  # noqa: E402
+from paper_1505_00344_b200 import systems, views  # noqa: E402
+from paper_1505_00344_b200._abi import FFError, FF_ERR_RANGE, FF_ERR_STATE, FF_ERR_UNKNOWN_SYMBOL  # noqa: E402
+
+LZ_LO, LZ_HI = [-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]   # Fig. 3A box
+LZ_P = np.array([10.0, 28.0, 8.0 / 3.0], np.float32)
+LAUNCHES = [(1, 128), (1, 256), (1, 512), (2, 128), (2, 256)]
+
+
+def lorenz_ctx(sizes, r=28.0):
+    ctx = FF.Context(systems.lorenz(), sizes)
+    ctx.set_param("r", r)
+    return ctx
+
+
+# ----------------------------------------------------------------------------- initial conditions
+def test_ic_bit_exact_and_padding_nan():
+    sizes = [5000, 3001, 1]
+    ctx = lorenz_ctx(sizes)
+    gs = [ctx.init_group(LZ_LO, LZ_HI, n, 1 if k != 1 else -1, 0, seed=2 + k) for k, n in enumerate(sizes)]
+    for k, (g, n) in enumerate(zip(gs, sizes)):
+        got = ctx.read_state(g)
+        want = O.ic_uniform(LZ_LO, LZ_HI, 2 + k, 0, n)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+        s, nl, _ = ctx.group_info(g)
+        pad = ctx.state[:, s + nl:s + ((nl + 511) // 512) * 512].cpu().numpy()
+        assert np.all(np.isnan(pad))
+
+
+def test_ic_golden_values():
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ic_golden.json")))
+    ctx = lorenz_ctx([4194305])
+    g = ctx.init_group(LZ_LO, LZ_HI, 4194305, 1, 0, seed=2)
+    for c in gold["ic"]:
+        x = ctx.read_state(g, c["index"], 1)[:, 0]
+        assert [int(b) for b in x.view(np.uint32)] == [int(b, 16) for b in c["bits"]]
+
+
+# ----------------------------------------------------------------------------- integrator parity
+@pytest.mark.parametrize("ppt,tpb", LAUNCHES)
+def test_lorenz_r28_tier_a_30_steps(ppt, tpb):
+    n = 20000 + 77  # several tiles and a ragged tail
+    ctx = lorenz_ctx([n, n])
+    ctx.set_launch(ppt, tpb)
+    gf = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=2)
+    gb = ctx.init_group(LZ_LO, LZ_HI, n, -1, 1, seed=3)
+    for _ in range(3):
+        ctx.step(10, 0.01)
+    sc = dim_scales(LZ_LO, LZ_HI)
+    for g, seed, h in ((gf, 2, 0.01), (gb, 3, -0.01)):
+        want = oracle_group(O.LORENZ, LZ_LO, LZ_HI, seed, 0, n, LZ_P, h, 30)
+        assert tier_a(ctx.read_state(g), want, sc) <= 1e-5
+
+
+def test_lorenz_r28_tier_b_100_steps():
+    n = 50000
+    ctx = lorenz_ctx([n])
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=2)
+    ctx.step(100, 0.01)
+    want = oracle_group(O.LORENZ, LZ_LO, LZ_HI, 2, 0, n, LZ_P, 0.01, 100)
+    got = ctx.read_state(g)
+    e = scaled_error(got, want, dim_scales(LZ_LO, LZ_HI)).max(axis=0)
+    assert np.percentile(e, 99) <= 1e-5 and np.percentile(e, 99.99) <= 1e-3
+
+
+def test_lorenz_r05_tier_a_1000_steps_and_origin_fixed():
+    n = 10000
+    ctx = lorenz_ctx([n, 512], r=0.5)
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=5)
+    g0 = ctx.init_group([0.0, 0.0, 0.0], [1e-30, 1e-30, 1e-30], 512, 1, 0, seed=6)
+    ctx.write_state(g0, np.zeros((3, 512), np.float32))
+    ctx.step(1000, 0.01)
+    p = np.array([10.0, 0.5, 8.0 / 3.0], np.float32)
+    want = oracle_group(O.LORENZ, LZ_LO, LZ_HI, 5, 0, n, p, 0.01, 1000)
+    assert tier_a(ctx.read_state(g), want, dim_scales(LZ_LO, LZ_HI)) <= 1e-5
+    assert np.all(ctx.read_state(g0) == 0)   # PAPER.md:87 fixed point, bit-exact
+
+
+def test_linear_closed_form_on_gpu():
+    # x' = -x, h = 0.1: one RK4 step is T4(-0.1) = 0.9048375, h = -0.1 -> 1.1051708
+    ctx = FF.Context(systems.linear([[-1.0]]), [512, 512])
+    g1 = ctx.init_group([1.0], [1.0000001], 512, 1, 0, 1)
+    g2 = ctx.init_group([1.0], [1.0000001], 512, -1, 0, 1)
+    ctx.write_state(g1, np.ones((1, 512), np.float32))
+    ctx.write_state(g2, np.ones((1, 512), np.float32))
+    ctx.step(1, 0.1)
+    assert np.allclose(ctx.read_state(g1), 0.9048375, rtol=2e-7, atol=0)
+    assert np.allclose(ctx.read_state(g2), 1.1051708333, rtol=2e-7, atol=0)
+
+
+def test_zero_steps_is_identity_and_params_take_effect():
+    n = 4096
+    ctx = lorenz_ctx([n], r=0.5)
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=9)
+    x0 = ctx.read_state(g)
+    ctx.step(0, 0.01)
+    assert np.array_equal(ctx.read_state(g), x0)
+    ctx.step(20, 0.01)
+    ctx.set_param("r", 28.0)  # the next launch sees the new value
+    ctx.step(10, 0.01)
+    want = O.rk4(O.LORENZ, x0, np.array([10, 0.5, 8 / 3], np.float32), np.float32(0.01), 20)
+    want = O.rk4(O.LORENZ, want, LZ_P, np.float32(0.01), 10)
+    assert tier_a(ctx.read_state(g), want, dim_scales(LZ_LO, LZ_HI)) <= 1e-5
+
+
+def stn_params():
+    s = systems.stn_gpe()
+    return np.array([p[1] for p in s.params], np.float32), s
+
+
+def test_stn_forward_1000_backward_100():
+    # Config 1 shape (BASELINE.json configs[0]): 5k forward + 5k backward, dt = 0.01.
+    p, s = stn_params()
+    ctx = FF.Context(s, [5000, 5000])
+    gf = ctx.init_group([0, 0], [1, 1], 5000, 1, 0, seed=1)
+    gb = ctx.init_group([0, 0], [1, 1], 5000, -1, 1, seed=11)
+    ctx.step(100, 0.01)
+    wb = oracle_group(O.STN, [0, 0], [1, 1], 11, 0, 5000, p, -0.01, 100)
+    assert tier_a(ctx.read_state(gb), wb, [1.0, 1.0]) <= 1e-5
+    ctx.step(900, 0.01)
+    wf = oracle_group(O.STN, [0, 0], [1, 1], 1, 0, 5000, p, 0.01, 1000)
+    assert tier_a(ctx.read_state(gf), wf, [1.0, 1.0]) <= 1e-5
+
+
+def test_stn_limit_cycle_tier_b():
+    p, s = stn_params()
+    p[0] = 7.8
+    ctx = FF.Context(s, [4000])
+    ctx.set_param("w_ss", 7.8)
+    g = ctx.init_group([0, 0], [1, 1], 4000, 1, 0, seed=3)
+    ctx.step(1000, 0.01)
+    want = oracle_group(O.STN, [0, 0], [1, 1], 3, 0, 4000, p, 0.01, 1000)
+    e = scaled_error(ctx.read_state(g), want, [1.0, 1.0]).max(axis=0)
+    assert np.percentile(e, 99) <= 1e-4 and e.max() <= 1e-3
+
+
+HH_LO = [-20.0, 0, 0, 0, 0] * 3
+HH_HI = [100.0, 1, 1, 1, 1] * 3
+
+
+def hh_params(s):
+    names = O.hh_param_names(3)
+    d = {p[0]: p[1] for p in s.params}
+    return np.array([d[k] for k in names], np.float32)
+
+
+@pytest.mark.parametrize("ppt", [1, 2])
+def test_hh_ring_tier_a_10_steps_tier_b_100(ppt):
+    s = systems.hh_ring(3)
+    p = hh_params(s)
+    n = 6000
+    ctx = FF.Context(s, [n])
+    ctx.set_launch(ppt, 256 if ppt == 1 else 128)
+    g = ctx.init_group(HH_LO, HH_HI, n, 1, 0, seed=4)
+    sc = dim_scales(HH_LO, HH_HI)
+    ctx.step(10, 0.01)
+    want = oracle_group(O.HH, HH_LO, HH_HI, 4, 0, n, p, 0.01, 10)
+    assert tier_a(ctx.read_state(g), want, sc) <= 1e-5
+    ctx.step(90, 0.01)
+    want = O.rk4(O.HH, want, p, np.float32(0.01), 90)
+    got = ctx.read_state(g)
+    same, both = finite_agreement(got, want)
+    assert same.all()
+    e = scaled_error(got[:, both], want[:, both], sc).max(axis=0)
+    assert np.percentile(e, 99) <= 1e-5 and e.max() <= 1e-3
+
+
+# ----------------------------------------------------------------------------- sweep
+@pytest.mark.parametrize("mode", [0, 1])
+def test_sweep_values_bit_exact_and_parity(mode):
+    n = 30000 + 5
+    ctx = lorenz_ctx([n])
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=5)
+    ctx.sweep_param(g, "r", 0.0, 200.0, mode, seed=5)
+    # the swept value is axis `dim` (= 3); a (r, r) window image pins every value bit-exactly
+    sv = O.sweep_values(0.0, 200.0, mode, 5, 0, n, n)
+    W = 4096
+    img = ctx.project([3, 3], [0.0, 200.0, 0.0, 200.0], W, 1, 1)
+    want = O.histogram(np.zeros((3, n), np.float32), [3, 3], [0.0, 200.0, 0.0, 200.0], W, 1, 1, 0, sweep_vals=sv)
+    assert np.array_equal(ctx.read_image(), want)
+    ctx.step(10, 0.01)
+    xo = O.rk4(O.LORENZ, O.ic_uniform(LZ_LO, LZ_HI, 5, 0, n), LZ_P, np.float32(0.01), 10, 1, sv)
+    assert tier_a(ctx.read_state(g), xo, dim_scales(LZ_LO, LZ_HI)) <= 1e-5
+    # lifted parameter unchanged: rebinning the swept axis after stepping gives the same image
+    img.zero_()
+    ctx.project([3, 3], [0.0, 200.0, 0.0, 200.0], W, 1, 1, image=img)
+    assert np.array_equal(ctx.read_image(), want)
+
+
+def test_sweep_and_param_errors():
+    ctx = lorenz_ctx([1000])
+    g = ctx.init_group(LZ_LO, LZ_HI, 1000, 1, 0, seed=5)
+    with pytest.raises(FFError) as e:
+        ctx.set_param("r", 1000.0)
+    assert e.value.status == FF_ERR_RANGE
+    with pytest.raises(FFError) as e:
+        ctx.set_param("bogus", 1.0)
+    assert e.value.status == FF_ERR_UNKNOWN_SYMBOL
+    ctx.sweep_param(g, "r", 0.0, 10.0)
+    with pytest.raises(FFError) as e:
+        ctx.sweep_param(g, "sigma", 0.0, 10.0)
+    assert e.value.status == FF_ERR_STATE
+
+
+# ----------------------------------------------------------------------------- histogram
+def special_state(n, rng):
+    x = np.vstack([rng.uniform(-12, 12, n), rng.uniform(-35, 35, n), rng.uniform(-5, 55, n)]).astype(np.float32)
+    k = n // 20
+    x[0, :k] = np.nan
+    x[1, k:2 * k] = np.inf
+    x[2, 2 * k:3 * k] = -np.inf
+    x[0, 3 * k:4 * k] = np.float32(1e-40)     # denormals (FTZ would change these)
+    x[1, 3 * k:4 * k] = np.float32(-1e-41)
+    x[0, 4 * k:5 * k] = -10.0                 # window edges
+    x[0, 5 * k:6 * k] = np.nextafter(np.float32(10.0), np.float32(0))
+    x[0, 6 * k:7 * k] = 10.0
+    return x
+
+
+@pytest.mark.parametrize("ppt,tpb", LAUNCHES)
+def test_histogram_2d_bit_exact_identical_state(ppt, tpb):
+    rng = np.random.default_rng(50)
+    n = 40000 + 13
+    ctx = lorenz_ctx([n])
+    ctx.set_launch(ppt, tpb)
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=1)
+    x = special_state(n, rng)
+    ctx.write_state(g, x)
+    view = [-10.0, 10.0, -30.0, 30.0]
+    ctx.project([0, 1], view, 333, 211, 2)   # odd sizes, colour 0 of 2 channels
+    want = O.histogram(x, [0, 1], view, 333, 211, 2, 0)
+    assert np.array_equal(ctx.read_image(), want)
+
+
+def test_histogram_3d_bit_exact_identical_state():
+    rng = np.random.default_rng(51)
+    n = 40000 + 13
+    ctx = lorenz_ctx([n, n])
+    g0 = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=1)
+    g1 = ctx.init_group(LZ_LO, LZ_HI, n, -1, 1, seed=2)
+    x0, x1 = special_state(n, rng), special_state(n, rng)
+    x1[1] = rng.uniform(-200, 50, n).astype(np.float32)   # some behind the camera
+    ctx.write_state(g0, x0)
+    ctx.write_state(g1, x1)
+    M = views.lorenz_camera()
+    ctx.project([0, 1, 2], M, 1024, 1024, 2)
+    want = O.histogram(x0, [0, 1, 2], M, 1024, 1024, 2, 0)
+    want = O.histogram(x1, [0, 1, 2], M, 1024, 1024, 2, 1, image=want)
+    assert np.array_equal(ctx.read_image(), want)
+
+
+def test_histogram_collapsed_regime_counts():
+    # All particles in one bin (Lorenz r < 1 attractor): counts must still be exact.
+    n = 100000
+    ctx = lorenz_ctx([n])
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=1)
+    ctx.write_state(g, np.zeros((3, n), np.float32))
+    img = ctx.project([0, 1], [-1.0, 1.0, -1.0, 1.0], 64, 64, 1)
+    im = ctx.read_image()
+    assert im.sum() == n and im[0, 32, 32] == n
+
+
+def test_fused_pipeline_matches_oracle_up_to_edge_particles():
+    n = 30000
+    ctx = lorenz_ctx([n])
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=2)
+    M = views.lorenz_camera()
+    img = ctx.project([0, 1, 2], M, 512, 512, 1)
+    img.zero_()
+    ctx.step(30, 0.01)   # fused: integrate then bin once
+    xo = oracle_group(O.LORENZ, LZ_LO, LZ_HI, 2, 0, n, LZ_P, 0.01, 30)
+    want = O.histogram(xo, [0, 1, 2], M, 512, 512, 1, 0)
+    got = ctx.read_image()
+    # particles whose oracle pixel coordinate is within 1e-3 px of a bin edge may land differently
+    X = xo.astype(np.float64)
+    Md = M.astype(np.float64)
+    c = Md @ np.vstack([X, np.ones((1, n))])
+    px, py = (c[0] / c[3] + 1) * 256, (c[1] / c[3] + 1) * 256
+    near = (np.abs(px - np.round(px)) < 1e-3) | (np.abs(py - np.round(py)) < 1e-3)
+    assert np.abs(got.astype(np.int64) - want.astype(np.int64)).sum() <= 2 * near.sum()
+    assert got.sum() == want.sum() or abs(int(got.sum()) - int(want.sum())) <= near.sum()
+
+
+# ----------------------------------------------------------------------------- sharding
+def test_shards_sum_to_whole():
+    # the image summed over shards equals the unsharded image bit-for-bit.
+    n = 25000 + 3
+    M = views.lorenz_camera()
+
+    def run(rank, world):
+        ctx = FF.Context(systems.lorenz(), [n, n], rank=rank, world=world)
+        ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=2)
+        ctx.init_group(LZ_LO, LZ_HI, n, -1, 1, seed=3)
+        img = ctx.project([0, 1, 2], M, 256, 256, 2)
+        img.zero_()
+        ctx.step(20, 0.01)
+        return ctx.read_image(), [ctx.read_state(k) for k in (0, 1)]
+
+    whole, sw = run(0, 1)
+    parts = [run(r, 3) for r in range(3)]
+    assert np.array_equal(sum(p[0].astype(np.uint64) for p in parts), whole.astype(np.uint64))
+    for k in (0, 1):
+        assert np.array_equal(np.hstack([p[1][k] for p in parts]), sw[k])
+
+
+def test_high_dim_system_compiles_and_matches():
+    # 20-D linear system exercises dim > 16 register tiers; closed form via the oracle's linear model
+    rng = np.random.default_rng(60)
+    A = (rng.normal(size=(20, 20)) * 0.1).astype(np.float32)
+    ctx = FF.Context(systems.linear(A.tolist()), [1000])
+    g = ctx.init_group([-1.0] * 20, [1.0] * 20, 1000, 1, 0, seed=7)
+    ctx.step(50, 0.01)
+    want = oracle_group(O.LINEAR, [-1.0] * 20, [1.0] * 20, 7, 0, 1000, A.ravel(), 0.01, 50)
+    assert tier_a(ctx.read_state(g), want, np.ones(20)) <= 1e-5
