@@ -43,7 +43,7 @@
 #define ORC_STN 3
 #define ORC_HH 4
 #define ORC_MAX_DIM 64
-#define ORC_MAX_PARAMS 128
+#define ORC_MAX_PARAMS 1024
 
 /* ---- float instantiation ---- */
 #define REAL float
@@ -145,8 +145,8 @@ int orc_ic_uniform_f32(const float* lo, const float* hi, int dim, uint64_t seed,
 
 /* Public: swept-parameter values (each particle has its own fixed value).
  * mode 0: Philox-uniform in [lo, hi) (stream 1, block 0, word 0);
- * mode 1: linspace, v_i = lo + (hi - lo) * ((i + 0.5) / n_group), computed as
- *         t = (float)(i + 0.5) / (float)n_group ... see DESIGN.md reading R13 for the exact ops. */
+ * mode 1: linspace, v_i = lo + (hi - lo) * u with u = (float)(((double)i + 0.5) / n_group), one
+ *         double division rounded once to float (reading R13). */
 int orc_sweep_values_f32(float lo, float hi, int mode, uint64_t seed, int64_t first, int64_t count,
                          int64_t n_group, float* out) {
   if (!(lo < hi) || count < 0 || first < 0 || n_group < 1 || first + count > n_group) return -1;
