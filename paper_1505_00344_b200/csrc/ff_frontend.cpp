@@ -309,8 +309,16 @@ struct Dag {
     if (is_num(x) && is_num(y)) return N(num(x) + num(y));
     if (is_num(x) && num(x) == 0.0) return y;
     if (is_num(y) && num(y) == 0.0) return x;
-    if (nodes[y].k == K::Neg) return sub(x, nodes[y].a[0]);
-    if (nodes[x].k == K::Neg) return sub(y, nodes[x].a[0]);
+    if (nodes[y].k == K::Neg && !nodes[y].uniform) return sub(x, nodes[y].a[0]);
+    if (nodes[x].k == K::Neg && !nodes[x].uniform) return sub(y, nodes[x].a[0]);
+    if (nodes[x].uniform && !nodes[y].uniform) std::swap(x, y);
+    if (nodes[y].uniform && !nodes[x].uniform) {
+      // (w + u1) + u2 -> w + (u1 + u2): uniform terms gather into one loop-invariant constant
+      const DNode& nx = nodes[x];
+      if (nx.k == K::Add && nodes[nx.a[1]].uniform) return add(nx.a[0], add(nx.a[1], y));
+      if (nx.k == K::Add && nodes[nx.a[0]].uniform) return add(nx.a[1], add(nx.a[0], y));
+      if (nx.k == K::Sub && nodes[nx.a[1]].uniform) return add(nx.a[0], sub(y, nx.a[1]));
+    }
     return op(K::Add, {x, y});
   }
   int sub(int x, int y) {
@@ -318,6 +326,7 @@ struct Dag {
     if (is_num(y) && num(y) == 0.0) return x;
     if (is_num(x) && num(x) == 0.0) return neg(y);
     if (nodes[y].k == K::Neg) return add(x, nodes[y].a[0]);
+    if (nodes[y].uniform && !nodes[x].uniform) return add(x, neg(y));
     // x - u*w with u uniform -> x + (-u)*w: the negation moves onto the loop-invariant factor, so
     // the packed path gets one FFMA2 (FFMA2 has no operand negation).
     if (nodes[y].k == K::Mul && !nodes[y].uniform) {
@@ -330,23 +339,23 @@ struct Dag {
   int mul(int x, int y) {
     if (is_num(x) && is_num(y)) return N(num(x) * num(y));
     if (is_num(y)) std::swap(x, y);  // constant first
+    if (nodes[y].uniform && !nodes[x].uniform) std::swap(x, y);  // uniform first
     if (is_num(x)) {
       const double c = num(x);
       if (c == 1.0) return y;
       if (c == -1.0) return neg(y);
+    }
+    if (nodes[x].uniform && !nodes[y].uniform) {
       const DNode& ny = nodes[y];
-      // c * (d * w) -> (c d) * w
-      if (ny.k == K::Mul && is_num(ny.a[0])) return mul(N(c * num(ny.a[0])), ny.a[1]);
-      // c * (-w) -> (-c) * w
-      if (ny.k == K::Neg) return mul(N(-c), ny.a[0]);
-      // c * (d +- w) -> c d +- c w (one FFMA instead of FADD + FMUL)
-      if ((ny.k == K::Add || ny.k == K::Sub) && is_num(ny.a[0])) {
-        int d = ny.a[0], w = ny.a[1];
-        return ny.k == K::Add ? add(N(c * num(d)), mul(N(c), w)) : sub(N(c * num(d)), mul(N(c), w));
-      }
-      if ((ny.k == K::Add || ny.k == K::Sub) && is_num(ny.a[1])) {
-        int w = ny.a[0], d = ny.a[1];
-        return ny.k == K::Add ? add(mul(N(c), w), N(c * num(d))) : sub(mul(N(c), w), N(c * num(d)));
+      // u1 * (u2 * w) -> (u1 u2) * w
+      if (ny.k == K::Mul && nodes[ny.a[0]].uniform) return mul(mul(x, ny.a[0]), ny.a[1]);
+      // u * (-w) -> (-u) * w
+      if (ny.k == K::Neg) return mul(neg(x), ny.a[0]);
+      // u * (w +- v) with one uniform term -> distribute: one FFMA instead of FADD + FMUL
+      if (ny.k == K::Add || ny.k == K::Sub) {
+        const int p = ny.a[0], q = ny.a[1];
+        if (nodes[p].uniform || nodes[q].uniform)
+          return ny.k == K::Add ? add(mul(x, p), mul(x, q)) : sub(mul(x, p), mul(x, q));
       }
     }
     return op(K::Mul, {x, y});
@@ -438,6 +447,203 @@ std::string flit(double v) {
   return s + "f";
 }
 
+
+// ---------------------------------------------------------------- sign-aware instruction selection
+// FFMA2 / FADD2 / FMUL2 (the packed pair path) have no operand negation, so every "-v" of a
+// varying value costs an instruction, while negating a uniform (loop-invariant) value is free. For
+// every varying node this computes the cheapest way to produce +v and -v (cost = packed FMA-pipe
+// instructions, FFMA fusion of single-use products included) and emits the chosen forms. The root of
+// a component may be produced negated; the integrator then uses negated step constants.
+struct Operand { int node; int neg; };
+struct Choice { enum Form { ADD, SUB, FMA, MUL, DIV, OTHER, NEGATE } form; Operand op[3]; };
+
+struct SignSelect {
+  const Dag& g;
+  const std::vector<char>& live;
+  std::vector<int> uses;
+  std::vector<double> c[2];
+  std::map<std::pair<int, int>, std::string> memo;
+  std::vector<std::string> uref;
+  std::ostringstream body;
+  int n_arith = 0, n_mufu = 0, tmp = 0;
+
+  SignSelect(const Dag& dag, const std::vector<char>& lv, const std::vector<int>& roots)
+      : g(dag), live(lv), uses(dag.nodes.size(), 0), uref(dag.nodes.size()) {
+    c[0].assign(g.nodes.size(), 0.0);
+    c[1].assign(g.nodes.size(), 0.0);
+    for (size_t id = 0; id < g.nodes.size(); ++id)
+      if (live[id])
+        for (int a : g.nodes[id].a) ++uses[a];
+    for (int r : roots) ++uses[r];
+    for (size_t id = 0; id < g.nodes.size(); ++id) {
+      if (!live[id]) continue;
+      Choice ch;
+      c[0][id] = best((int)id, 0, ch);
+      c[1][id] = best((int)id, 1, ch);
+    }
+  }
+
+  double cost(int id, int s) const { return c[s][id]; }
+  bool fusable(int id) const {
+    const DNode& n = g.nodes[id];
+    return n.k == K::Mul && !n.uniform && uses[id] == 1;
+  }
+  // cheapest factor signs (sx, sy) with sx xor sy = s for the product node m
+  double prod(int m, int s, Operand& x, Operand& y) const {
+    const int a = g.nodes[m].a[0], b = g.nodes[m].a[1];
+    double bestc = 1e30;
+    x = {a, 0};
+    y = {b, s};
+    for (int sa = 0; sa < 2; ++sa) {
+      const int sb = sa ^ s;
+      const double v = c[sa][a] + c[sb][b];
+      if (v < bestc) { bestc = v; x = {a, sa}; y = {b, sb}; }
+    }
+    return bestc;
+  }
+
+  double best(int id, int s, Choice& ch) const {
+    const DNode& n = g.nodes[id];
+    if (n.uniform) return 0.0;
+    const double INF = 1e30;
+    double bc = INF;
+    auto consider = [&](double v, Choice cand) { if (v < bc) { bc = v; ch = cand; } };
+    switch (n.k) {
+      case K::Var: return s ? 1.0 : 0.0;
+      case K::Sweep: return 0.0;
+      case K::Neg: return c[s ^ 1][n.a[0]];
+      case K::Add:
+      case K::Sub: {
+        const int a = n.a[0], b = n.a[1];
+        const int sb = n.k == K::Add ? s : (s ^ 1);  // value = (s a) + (sb b)
+        consider(1 + c[s][a] + c[sb][b], {Choice::ADD, {{a, s}, {b, sb}, {}}});
+        consider(1 + c[s][a] + c[sb ^ 1][b], {Choice::SUB, {{a, s}, {b, sb ^ 1}, {}}});
+        consider(1 + c[sb][b] + c[s ^ 1][a], {Choice::SUB, {{b, sb}, {a, s ^ 1}, {}}});
+        Operand x, y;
+        if (fusable(a)) { double v = 1 + prod(a, s, x, y) + c[sb][b]; consider(v, {Choice::FMA, {x, y, {b, sb}}}); }
+        if (fusable(b)) { double v = 1 + prod(b, sb, x, y) + c[s][a]; consider(v, {Choice::FMA, {x, y, {a, s}}}); }
+        break;
+      }
+      case K::Mul: {
+        Operand x, y;
+        double v = 1 + prod(id, s, x, y);
+        consider(v, {Choice::MUL, {x, y, {}}});
+        break;
+      }
+      case K::Div: {  // a * rcp(b): rcp(-b) = -rcp(b)
+        const int a = n.a[0], b = n.a[1];
+        for (int sa = 0; sa < 2; ++sa)
+          consider(2 + c[sa][a] + c[sa ^ s][b], {Choice::DIV, {{a, sa}, {b, sa ^ s}, {}}});
+        break;
+      }
+      case K::Rcp:
+        consider(1 + c[s][n.a[0]], {Choice::OTHER, {{n.a[0], s}, {}, {}}});
+        break;
+      default: {
+        double v = 1;
+        for (int x : n.a) v += c[0][x];
+        if (s == 0) consider(v, {Choice::OTHER, {}});
+        else consider(v + 1, {Choice::NEGATE, {}});
+      }
+    }
+    return bc;
+  }
+
+  std::string ureference(int id) {
+    if (!uref[id].empty()) return uref[id];
+    const DNode& n = g.nodes[id];
+    auto A = [&](int j) { return ureference(n.a[j]); };
+    std::string e;
+    switch (n.k) {
+      case K::Num: return uref[id] = flit(n.value);
+      case K::Param: return uref[id] = "a.p[" + std::to_string(n.index) + "]";
+      default: e = expr(n, A); break;
+    }
+    std::string name = "u" + std::to_string(id);
+    body << "  const float " << name << " = " << e << ";\n";
+    return uref[id] = name;
+  }
+
+  template <class F>
+  std::string expr(const DNode& n, F A) {
+    switch (n.k) {
+      case K::Neg: return "-" + A(0);
+      case K::Add: return A(0) + " + " + A(1);
+      case K::Sub: return A(0) + " - " + A(1);
+      case K::Mul: return A(0) + " * " + A(1);
+      case K::Rcp: return "ff_rcp(" + A(0) + ")";
+      case K::Div: return "ff_div(" + A(0) + ", " + A(1) + ")";
+      case K::Exp2: return "ff_exp2(" + A(0) + ")";
+      case K::Log: return "ff_log(" + A(0) + ")";
+      case K::Sin: return "ff_sin(" + A(0) + ")";
+      case K::Cos: return "ff_cos(" + A(0) + ")";
+      case K::Tan: return "ff_tan(" + A(0) + ")";
+      case K::Tanh: return "ff_tanh(" + A(0) + ")";
+      case K::Sqrt: return "ff_sqrt(" + A(0) + ")";
+      case K::Abs: return "ff_abs(" + A(0) + ")";
+      case K::Min: return "ff_min(" + A(0) + ", " + A(1) + ")";
+      case K::Max: return "ff_max(" + A(0) + ", " + A(1) + ")";
+      case K::Pow: return "ff_pow(" + A(0) + ", " + A(1) + ")";
+      case K::Sigmoid2: return "ff_rcp(1.0f + ff_exp2(" + A(0) + "))";
+      case K::Vtrap: return "ff_vtrap(" + A(0) + ", " + A(1) + ", " + A(2) + ")";
+      default: throw Error(FF_ERR_COMPILE, "internal: unexpected node in expr()");
+    }
+  }
+
+  std::string get(Operand o) { return get(o.node, o.neg); }
+
+  // reference to an expression equal to (s ? -v : v)
+  std::string get(int id, int s) {
+    const DNode& n = g.nodes[id];
+    if (n.uniform) return s ? "(-" + ureference(id) + ")" : ureference(id);
+    if (n.k == K::Neg) return get(n.a[0], s ^ 1);
+    if (n.k == K::Sweep) return s ? "nsw" : "sw";
+    if (n.k == K::Var && s == 0) return "x[" + std::to_string(n.index) + "]";
+    auto key = std::make_pair(id, s);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    std::string e;
+    if (n.k == K::Var) {
+      e = "-x[" + std::to_string(n.index) + "]";
+      ++n_arith;
+    } else {
+      Choice ch;
+      best(id, s, ch);
+      switch (ch.form) {
+        case Choice::ADD: e = get(ch.op[0]) + " + " + get(ch.op[1]); ++n_arith; break;
+        case Choice::SUB: e = get(ch.op[0]) + " - " + get(ch.op[1]); ++n_arith; break;
+        case Choice::MUL: e = get(ch.op[0]) + " * " + get(ch.op[1]); ++n_arith; break;
+        case Choice::FMA: e = "ff_fma(" + get(ch.op[0]) + ", " + get(ch.op[1]) + ", " + get(ch.op[2]) + ")"; ++n_arith; break;
+        case Choice::DIV: e = "ff_div(" + get(ch.op[0]) + ", " + get(ch.op[1]) + ")"; ++n_arith; ++n_mufu; break;
+        case Choice::OTHER:
+          if (n.k == K::Rcp) { e = "ff_rcp(" + get(ch.op[0]) + ")"; ++n_mufu; break; }
+          e = expr(n, [&](int j) { return get(n.a[j], 0); });
+          count(n);
+          break;
+        case Choice::NEGATE:
+          e = "-" + get(id, 0);
+          ++n_arith;
+          break;
+      }
+    }
+    std::string name = "t" + std::to_string(tmp++);
+    body << "  const V " << name << " = " << e << ";\n";
+    memo[key] = name;
+    return name;
+  }
+
+  void count(const DNode& n) {
+    switch (n.k) {
+      case K::Exp2: case K::Log: case K::Sin: case K::Cos: case K::Tanh: case K::Sqrt: ++n_mufu; break;
+      case K::Tan: n_mufu += 3; break;
+      case K::Pow: n_mufu += 2; ++n_arith; break;
+      case K::Sigmoid2: n_mufu += 2; ++n_arith; break;
+      case K::Vtrap: n_mufu += 2; n_arith += 9; break;
+      default: ++n_arith;
+    }
+  }
+};
+
 }  // namespace
 
 std::string emit_source(const System& s, int sweep_param) {
@@ -456,45 +662,15 @@ std::string emit_source(const System& s, int sweep_param) {
   };
   for (int r : roots) mark(r);
 
-  std::vector<std::string> ref(g.nodes.size());
-  std::ostringstream body;
-  int n_mufu = 0, n_arith = 0;
-  for (size_t id = 0; id < g.nodes.size(); ++id) {
-    if (!live[id]) continue;
-    const DNode& n = g.nodes[id];
-    auto A = [&](int j) { return ref[n.a[j]]; };
-    std::string e;
-    switch (n.k) {
-      case K::Num: ref[id] = flit(n.value); continue;
-      case K::Var: ref[id] = "x[" + std::to_string(n.index) + "]"; continue;
-      case K::Param: ref[id] = "a.p[" + std::to_string(n.index) + "]"; continue;
-      case K::Sweep: ref[id] = "sw"; continue;
-      case K::Neg: e = "-" + A(0); break;
-      case K::Add: e = A(0) + " + " + A(1); ++n_arith; break;
-      case K::Sub: e = A(0) + " - " + A(1); ++n_arith; break;
-      case K::Mul: e = A(0) + " * " + A(1); ++n_arith; break;
-      case K::Rcp: e = "ff_rcp(" + A(0) + ")"; ++n_mufu; break;
-      case K::Div: e = "ff_div(" + A(0) + ", " + A(1) + ")"; ++n_mufu; ++n_arith; break;
-      case K::Exp2: e = "ff_exp2(" + A(0) + ")"; ++n_mufu; break;
-      case K::Log: e = "ff_log(" + A(0) + ")"; ++n_mufu; break;
-      case K::Sin: e = "ff_sin(" + A(0) + ")"; ++n_mufu; break;
-      case K::Cos: e = "ff_cos(" + A(0) + ")"; ++n_mufu; break;
-      case K::Tan: e = "ff_tan(" + A(0) + ")"; n_mufu += 3; break;
-      case K::Tanh: e = "ff_tanh(" + A(0) + ")"; ++n_mufu; break;
-      case K::Sqrt: e = "ff_sqrt(" + A(0) + ")"; ++n_mufu; break;
-      case K::Abs: e = "ff_abs(" + A(0) + ")"; break;
-      case K::Min: e = "ff_min(" + A(0) + ", " + A(1) + ")"; break;
-      case K::Max: e = "ff_max(" + A(0) + ", " + A(1) + ")"; break;
-      case K::Pow: e = "ff_pow(" + A(0) + ", " + A(1) + ")"; n_mufu += 2; break;
-      case K::Sigmoid2: e = "ff_rcp(1.0f + ff_exp2(" + A(0) + "))"; n_mufu += 2; ++n_arith; break;
-      case K::Vtrap: e = "ff_vtrap(" + A(0) + ", " + A(1) + ", " + A(2) + ")"; n_mufu += 2; n_arith += 9; break;
-    }
-    // uniform nodes depend on parameters/constants only: `float`, loop-invariant (hoisted)
-    const char* ty = n.uniform ? "float" : "V";
-    std::string name = (n.uniform ? "u" : "t") + std::to_string(id);
-    body << "  const " << ty << " " << name << " = " << e << ";\n";
-    ref[id] = name;
+  SignSelect sel(g, live, roots);
+  std::vector<int> sign(s.dim, 1);
+  std::vector<std::string> out(s.dim);
+  for (int i = 0; i < s.dim; ++i) {
+    const int r = roots[i];
+    if (!g.nodes[r].uniform && sel.cost(r, 1) < sel.cost(r, 0)) sign[i] = -1;
+    out[i] = sel.get(r, sign[i] < 0 ? 1 : 0);
   }
+  const int n_arith = sel.n_arith, n_mufu = sel.n_mufu;
   std::ostringstream rhs;
   rhs << "// Generated right-hand side (" << s.dim << " state variables, " << s.param_names.size()
       << " parameters, swept parameter index " << sweep_param << ").\n";
@@ -506,12 +682,19 @@ std::string emit_source(const System& s, int sweep_param) {
   rhs << "template <class V>\n__device__ __forceinline__ void ff_rhs(const V* __restrict__ x, V* __restrict__ dx, "
          "const FFStepArgs& a, const V& sw) {\n";
   rhs << "  (void)a; (void)sw;\n";
-  rhs << body.str();
+  rhs << "  const V nsw = -sw; (void)nsw;\n";
+  rhs << sel.body.str();
   for (int i = 0; i < s.dim; ++i) {
     const DNode& r = g.nodes[roots[i]];
-    rhs << "  dx[" << i << "] = " << (r.uniform ? "ff_bcast<V>(" + ref[roots[i]] + ")" : ref[roots[i]]) << ";\n";
+    rhs << "  dx[" << i << "] = " << (r.uniform ? "ff_bcast<V>(" + out[i] + ")" : out[i]) << ";"
+        << (sign[i] < 0 ? "  // = -d" + s.var_names[i] + "/dt (FF_SIGN)" : "") << "\n";
   }
   rhs << "}\n";
+  rhs << "// dx[d] holds FF_SIGN[d] * f_d(x): a component computed negated saves FFMA2 negations; the\n"
+         "// integrator folds the sign into its (uniform) step constants.\n";
+  rhs << "__device__ constexpr float FF_SIGN[FF_DIM] = {";
+  for (int i = 0; i < s.dim; ++i) rhs << (i ? ", " : "") << (sign[i] < 0 ? "-1.0f" : "1.0f");
+  rhs << "};\n";
 
   const int dim = s.dim;
   const int unroll = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);

@@ -1,0 +1,7 @@
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -2
+timeout 900 python -m pytest tests -m gpu -q -rf 2>&1 | tail -5
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/r01_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ff_step -s 3 -c 1 -o gpurun_out/prof_p1 python bench.py --steps 1 --warmup 3 --ppt 1 --tpb 256 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ff_step -s 3 -c 1 -o gpurun_out/prof_p2 python bench.py --steps 1 --warmup 3 --ppt 2 --tpb 256 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ff_step -s 3 -c 1 -o gpurun_out/prof_s1 python bench.py --steps 1 --warmup 3 --S 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+ls -la gpurun_out/
