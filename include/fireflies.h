@@ -117,6 +117,11 @@ ff_status ff_set_stream(ff_ctx* ctx, void* cuda_stream);
  * Must be called before the first ff_init_group. Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE. */
 ff_status ff_set_shard(ff_ctx* ctx, int rank, int world);
 
+/* Host-only (no context, no device): the contiguous index range [*first, *first + *count) of a
+ * group of n_global particles held by shard `rank` of `world` (the rule of ff_set_shard).
+ * Errors: FF_ERR_INVALID_ARG. */
+ff_status ff_shard_range(int64_t n_global, int rank, int world, int64_t* first, int64_t* count);
+
 /* Bind caller-owned particle state: device pointer to float[dim][pitch] (SoA: component d of
  * slot j at state[d*pitch + j]), 16-byte aligned, pitch a multiple of FF_TILE, capacity <= pitch
  * slots usable. Must be called before the first ff_init_group (rebinding clears the groups).

@@ -20,7 +20,7 @@ FF_MAX_GROUPS = 16
 
 # Every symbol include/fireflies.h declares (checked by tests/test_abi.py).
 EXPORTS = ["ff_last_error", "ff_abi_version", "ff_emit_source", "ff_compile_cubin", "ff_create", "ff_destroy",
-           "ff_set_stream", "ff_set_shard", "ff_bind_state", "ff_group_slots", "ff_init_group", "ff_group_info",
+           "ff_set_stream", "ff_set_shard", "ff_shard_range", "ff_bind_state", "ff_group_slots", "ff_init_group", "ff_group_info",
            "ff_set_param", "ff_get_param", "ff_sweep_param", "ff_project", "ff_step", "ff_set_launch",
            "ff_read_state", "ff_write_state", "ff_read_image", "ff_launch_count", "ff_sync"]
 
@@ -60,6 +60,7 @@ def lib():
             "ff_destroy": ([P], C.c_int),
             "ff_set_stream": ([P, P], C.c_int),
             "ff_set_shard": ([P, i32, i32], C.c_int),
+            "ff_shard_range": ([i64, i32, i32, C.POINTER(i64), C.POINTER(i64)], C.c_int),
             "ff_bind_state": ([P, P, i64, i64], C.c_int),
             "ff_group_slots": ([P, i64, C.POINTER(i64)], C.c_int),
             "ff_init_group": ([P, P, P, i64, i32, i32, u64, C.POINTER(i32)], C.c_int),

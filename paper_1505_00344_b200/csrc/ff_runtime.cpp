@@ -122,8 +122,10 @@ struct ff_ctx {
   }
 
   void default_launch(int& ppt_out, int& tpb_out) const {
-    ppt_out = ppt ? ppt : (sys.dim <= 8 ? 2 : 1);
-    tpb_out = tpb ? tpb : 256;
+    // measured on B200: packed pairs win for the paper's systems; 15-D HH needs the
+    // smaller block for its ~248-register pair kernel
+    ppt_out = ppt ? ppt : (sys.dim <= 16 ? 2 : 1);
+    tpb_out = tpb ? tpb : (sys.dim <= 8 ? 256 : 128);
   }
 
   void launch_step(int64_t n_steps, float dt) {
@@ -306,6 +308,16 @@ ff_status ff_bind_state(ff_ctx* ctx, float* dev_state, int64_t pitch, int64_t ca
 
 static int64_t shard_begin(int64_t n, int r, int w) { return (int64_t)((__int128)n * r / w); }
 
+ff_status ff_shard_range(int64_t n_global, int rank, int world, int64_t* first, int64_t* count) {
+  FF_TRY
+  need(first && count, FF_ERR_INVALID_ARG, "NULL argument");
+  need(n_global >= 0, FF_ERR_INVALID_ARG, "n_global must be >= 0");
+  need(world >= 1 && rank >= 0 && rank < world, FF_ERR_INVALID_ARG, "need 0 <= rank < world");
+  *first = shard_begin(n_global, rank, world);
+  *count = shard_begin(n_global, rank + 1, world) - *first;
+  FF_CATCH
+}
+
 ff_status ff_group_slots(ff_ctx* ctx, int64_t n_global, int64_t* slots) {
   FF_TRY
   need(ctx && slots, FF_ERR_INVALID_ARG, "NULL argument");
@@ -468,10 +480,16 @@ ff_status ff_set_launch(ff_ctx* ctx, int ppt, int tpb) {
   need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
   need(ppt == 0 || ppt == 1 || ppt == 2, FF_ERR_INVALID_ARG, "particles per thread must be 0, 1 or 2");
   need(tpb == 0 || tpb == 128 || tpb == 256 || tpb == 512, FF_ERR_INVALID_ARG, "threads per block must be 0/128/256/512");
-  int p = ppt ? ppt : (ctx->sys.dim <= 8 ? 2 : 1), t = tpb ? tpb : 256;
-  need(step_index(p, t) >= 0, FF_ERR_INVALID_ARG, "unsupported (ppt, tpb) combination");
+  const int old_p = ctx->ppt, old_t = ctx->tpb;
   ctx->ppt = ppt;
   ctx->tpb = tpb;
+  int p, t;
+  ctx->default_launch(p, t);
+  if (step_index(p, t) < 0) {
+    ctx->ppt = old_p;
+    ctx->tpb = old_t;
+    throw ff::Error(FF_ERR_INVALID_ARG, "unsupported (ppt, tpb) combination");
+  }
   FF_CATCH
 }
 

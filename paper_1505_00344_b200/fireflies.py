@@ -64,6 +64,12 @@ def ff_set_shard(ctx, rank: int, world: int):
     check(lib().ff_set_shard(ctx, rank, world))
 
 
+def ff_shard_range(n_global: int, rank: int, world: int):
+    first, count = C.c_int64(), C.c_int64()
+    check(lib().ff_shard_range(n_global, rank, world, C.byref(first), C.byref(count)))
+    return first.value, count.value
+
+
 def ff_bind_state(ctx, dev_ptr: int, pitch: int, capacity: int):
     check(lib().ff_bind_state(ctx, C.c_void_p(dev_ptr), pitch, capacity))
 
