@@ -51,6 +51,10 @@ WORKLOADS = {
                   box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj=([3, 1], [0.0, 200.0, -160.0, 160.0]),
                   W=2048, H=1024, C=1, S=100, dt=0.01, fma_ops=45, mufu_ops=0, bound="alu",
                   desc="Lorenz r swept in [0,200), 16M particles, (r, y) image 2048x1024 (configs[3])"),
+    "lorenz3d_collapsed": dict(system="lorenz", groups=[(1 << 22, 1, 0, 2), (1 << 22, 1, 1, 3)], params={"r": 0.5},
+                               box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj="lorenz_camera", W=1024, H=1024,
+                               C=2, S=100, dt=0.01, fma_ops=45, mufu_ops=0, bound="alu", prerun=4000,
+                               desc="Lorenz r=0.5 after 4000 steps: 8M particles in ~1 pixel (histogram stress)"),
     "lorenz1b": dict(system="lorenz", groups=[(1 << 30, 1, 0, 6)], params={"r": 28.0}, strong=True,
                      box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj="lorenz_camera", W=1024, H=1024, C=1,
                      S=100, dt=0.01, fma_ops=45, mufu_ops=0, bound="alu",
@@ -142,6 +146,8 @@ def run_ours(args, w, rank, world, device):
         name, a, b, mode, seed = w["sweep"]
         for g in gids:
             ctx.sweep_param(g, name, a, b, mode, seed)
+    if w.get("prerun"):
+        ctx.step(w["prerun"], w["dt"])
     axes, view = projection(w)
     img = ctx.project(axes, view, w["W"], w["H"], w["C"])
     n_local = sum(ctx.group_info(g)[1] for g in gids)

@@ -291,6 +291,34 @@ def test_histogram_collapsed_regime_counts():
     assert im.sum() == n and im[0, 32, 32] == n
 
 
+@pytest.mark.parametrize("ppt,tpb", [(1, 256), (2, 256), (2, 128)])
+def test_histogram_aggregation_regimes_exact(ppt, tpb):
+    # Runs of 8 equal bins (warp aggregation + block hash table) over ~6k distinct bins (more than
+    # the 1024-entry table holds: overflow path), two hot pixels holding half the particles, and
+    # scattered particles (direct path) -- all in one image, checked bit-exactly.
+    n = 50000 + 3
+    rng = np.random.default_rng(52)
+    ctx = lorenz_ctx([n])
+    ctx.set_launch(ppt, tpb)
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=1)
+    W, H = 300, 200
+    ix = np.repeat(rng.integers(0, W, n // 8 + 1), 8)[:n]
+    iy = np.repeat(rng.integers(0, H, n // 8 + 1), 8)[:n]
+    hot = rng.random(n) < 0.5
+    ix[hot], iy[hot] = np.where(rng.random(hot.sum()) < 0.5, 7, 250), 100
+    scat = rng.random(n) < 0.1
+    ix[scat], iy[scat] = rng.integers(0, W, scat.sum()), rng.integers(0, H, scat.sum())
+    x = np.zeros((3, n), np.float32)
+    x[0] = (-10.0 + (ix + 0.5) * (20.0 / W)).astype(np.float32)
+    x[1] = (-30.0 + (iy + 0.5) * (60.0 / H)).astype(np.float32)
+    ctx.write_state(g, x)
+    view = [-10.0, 10.0, -30.0, 30.0]
+    ctx.project([0, 1], view, W, H, 1)
+    want = O.histogram(x, [0, 1], view, W, H, 1, 0)
+    assert np.array_equal(ctx.read_image(), want)
+    assert want[0, 100, 7] > n // 5
+
+
 def test_fused_pipeline_matches_oracle_up_to_edge_particles():
     n = 30000
     ctx = lorenz_ctx([n])
