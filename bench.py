@@ -150,9 +150,14 @@ def run_ours(args, w, rank, world, device):
         ctx.step(w["prerun"], w["dt"])
     axes, view = projection(w)
     img = ctx.project(axes, view, w["W"], w["H"], w["C"])
+    if args.no_image:   # integration only (HBM roofline of single-step launches without binning)
+        ctx.unbind_image()
     n_local = sum(ctx.group_info(g)[1] for g in gids)
     stream = ctx.stream
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)   # > 126 MB L2
+    # L2 flush = READ 256 MiB (> 126 MB L2) so the cache is refilled with clean lines: a memset would
+    # leave ~126 MB of dirty lines whose write-back the next timed kernel would pay for
+    flush = torch.ones(64 << 20, dtype=torch.float32, device=device)
+    flush_sink = torch.empty((), dtype=torch.float32, device=device)
     dist = world > 1
 
     def frame():
@@ -172,7 +177,7 @@ def run_ours(args, w, rank, world, device):
     with ClockSampler(device.index) as clk:
         t_wall = time.perf_counter()
         for i in range(args.steps):
-            flush.zero_()                       # L2 flush between timed iterations (not timed)
+            torch.sum(flush, out=flush_sink)    # L2 flush between timed iterations (not timed)
             ev[i][0].record(stream)
             img.zero_()
             ev[i][1].record(stream)
@@ -230,9 +235,21 @@ def run_ours(args, w, rank, world, device):
                "d2h_bytes_per_step": d2h, "ms_per_step": ms}
     im_sum = int(img.sum().item())
     ctx.close()
-    return dict(S=S, n_total=n_total, n_local=n_local, t_total_ms=t_total, kern_ms=kern_mean,
+    sweep_idx = -1
+    if "sweep" in w:
+        sweep_idx = [p[0] for p in make_system(w["system"]).params].index(w["sweep"][0])
+    return dict(S=S, n_total=n_total, n_local=n_local, sweep_idx=sweep_idx, t_total_ms=t_total, kern_ms=kern_mean,
                 frame_ms=frame_ms, launches=launches, clocks=clk.summary(), e2e=e2e, image_sum=im_sum,
                 t_wall=t_wall)
+
+
+def op_counts(sysdef, sweep_idx):
+    """(FMA-pipe lane-ops, MUFU ops) per particle-step of the generated kernel (front-end count)."""
+    import re
+    import paper_1505_00344_b200 as FF
+    src = FF.ff_emit_source(sysdef, sweep_idx)
+    m = re.search(r"per evaluation \(front-end count\): (\d+) arithmetic ops, (\d+) MUFU ops", src)
+    return 4 * int(m.group(1)) + 7 * sysdef.dim, 4 * int(m.group(2))
 
 
 def cpu_oracle_sample(w, n_sample, S):
@@ -280,6 +297,7 @@ def main():
     ap.add_argument("--ppt", type=int, default=0)
     ap.add_argument("--tpb", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-image", action="store_true", help="do not bind the image (integration only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -290,7 +308,7 @@ def main():
     S = args.S or w["S"]
     config = {"workload": args.config, "description": w["desc"], "steps_per_frame": S, "dt": w["dt"],
               "particles_per_gpu": (sum(g[0] for g in w["groups"]) // (world if w.get("strong") else 1)),
-              "image": [w["C"], w["H"], w["W"]], "l2": "flushed between timed frames (256 MiB memset)",
+              "image": [w["C"], w["H"], w["W"]], "l2": "flushed between timed frames (256 MiB read, outside the timed events)",
               "parallelism": f"particles sharded over {world} GPU(s), NCCL image all-reduce per frame"
               if world > 1 else "1 GPU"}
 
@@ -333,21 +351,29 @@ def main():
     f_max = (peaks.get("sm_max_mhz") or clocks.get("sm_max_mhz") or 1965.0) * 1e6
     kern_s = r["kern_ms"] * 1e-3
     per_launch = r["n_local"] * r["S"]
-    if w["bound"] == "alu":
-        achieved = per_launch * w["fma_ops"] / kern_s
-        peak = N_SM * FMA_LANES * f_max
-        roof = {"bound": "alu", "unit": "Tops/s (FP32 FMA-pipe lane-ops, FMA = 1 op)",
-                "achieved": achieved / 1e12, "peak": peak / 1e12, "frac": achieved / peak,
-                "peak_source": f"148 SM x 128 FP32 lanes x {f_max / 1e6:.0f} MHz (MEASURED_PEAKS sm_max_mhz; "
-                               "B200_PROFILING.md unit counts; FFMA2 measured at 128 lanes/clk)",
-                "alg_ops_per_particle_step": w["fma_ops"]}
-    else:
-        achieved = per_launch * w["mufu_ops"] / kern_s
-        peak = N_SM * XU_LANES * f_max
-        roof = {"bound": "alu", "pipe": "xu", "unit": "Tops/s (MUFU ex2/rcp results)",
-                "achieved": achieved / 1e12, "peak": peak / 1e12, "frac": achieved / peak,
-                "peak_source": f"148 SM x 16 MUFU/clk x {f_max / 1e6:.0f} MHz (profiles/r01_ubench_pipes.txt)",
-                "alg_ops_per_particle_step": w["mufu_ops"]}
+    # Work per particle-step from the front end's own count of the generated RHS (4 evaluations) plus
+    # the RK4 combination (7 FMA-pipe ops per dimension); Lorenz: 4 x 6 + 3 x 7 = 45.
+    sysdef = make_system(w["system"])
+    fma_ops, mufu_ops = op_counts(sysdef, r["sweep_idx"])
+    dim = sysdef.dim
+    cands = {
+        "fma": (per_launch * fma_ops / kern_s, N_SM * FMA_LANES * f_max,
+                "Tops/s (FP32 FMA-pipe lane-ops, a*b+c = 1 op)",
+                f"148 SM x 128 FP32 lanes x {f_max / 1e6:.0f} MHz (MEASURED_PEAKS sm_max_mhz; FFMA2 measured at "
+                "128 lanes/clk, profiles/r01_ubench_pipes.txt)", fma_ops),
+        "xu": (per_launch * mufu_ops / kern_s, N_SM * XU_LANES * f_max, "Tops/s (MUFU ex2/rcp results)",
+               f"148 SM x 16 MUFU/clk x {f_max / 1e6:.0f} MHz (profiles/r01_ubench_pipes.txt)", mufu_ops),
+        "hbm": (r["n_local"] * 8 * dim / kern_s, peaks.get("hbm_gbs", 6549.1) * 1e9, "GB/s",
+                "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)", 8 * dim / r["S"]),
+    }
+    fracs = {k: v[0] / v[1] for k, v in cands.items()}
+    pipe = max(fracs, key=fracs.get)
+    ach, peak, unit, src, per_unit = cands[pipe]
+    scale = 1e9 if pipe == "hbm" else 1e12
+    roof = {"bound": "hbm" if pipe == "hbm" else "alu", "pipe": pipe, "unit": unit, "achieved": ach / scale,
+            "peak": peak / scale, "frac": ach / peak, "peak_source": src,
+            "alg_per_particle_step": per_unit, "fracs_all_pipes": fracs,
+            "kernel": "ff_step (integrate S steps + project + count, one launch)"}
     roof["traffic"] = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -360,7 +386,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": r["t_total_ms"] / args.steps, "higher_is_better": True,
             "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Philox ICs from the paper's IC boxes)", "config": config,
-            "pct_fp32_peak": 100 * roof["frac"] if w["bound"] == "alu" else None,
+            "pct_fp32_peak": 100 * fracs["fma"],
             "roofline": roof, "clocks": clocks, "gpu_launches": r["launches"], "e2e": r["e2e"],
             "kernel_ms_mean": r["kern_ms"], "frame_ms_p10_p50_p90": [float(np.percentile(r["frame_ms"], q))
                                                                      for q in (10, 50, 90)],

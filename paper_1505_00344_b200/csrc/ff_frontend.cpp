@@ -250,7 +250,8 @@ namespace {
 enum class K {
   Num, Var, Param, Sweep,
   Neg, Add, Sub, Mul, Rcp, Div,
-  Exp2, Log, Sin, Cos, Tan, Tanh, Sqrt, Abs, Min, Max, Pow, Sigmoid2, Vtrap
+  Exp2, Log, Sin, Cos, Tan, Tanh, Sqrt, Abs, Min, Max, Pow, Sigmoid2, Vtrap,
+  SelAbsLt  // |a0| < value ? a1 : a2 (branch-free select)
 };
 
 struct DNode {
@@ -265,13 +266,18 @@ struct Dag {
   std::vector<DNode> nodes;
   std::unordered_map<std::string, int> memo;
   int sweep_param;
+  // exp sharing (see exp_): pass 1 records (signature of w, c) for every 2^(c w + d); pass 2 gets a
+  // plan {signature -> base coefficient c0} and derives 2^(c w + d) = 2^d (2^(c0 w))^(c/c0).
+  const std::map<std::string, double>* plan = nullptr;
+  std::vector<std::pair<std::string, std::pair<double, double>>> exp_uses;
+  std::unordered_map<int, std::string> sigmemo;
 
   explicit Dag(int sp) : sweep_param(sp) {}
 
   int intern(DNode n) {
     std::ostringstream key;
     key << (int)n.k << ':';
-    if (n.k == K::Num) {
+    {
       uint64_t bits;
       std::memcpy(&bits, &n.value, 8);
       key << bits;
@@ -334,6 +340,14 @@ struct Dag {
       if (nodes[u].uniform) return add(x, mul(neg(u), w));
       if (nodes[w].uniform) return add(x, mul(neg(w), u));
     }
+    // u - (w + v), u - (w - v), u - (v - w) with u, v uniform: gather the uniform terms
+    if (nodes[x].uniform && !nodes[y].uniform && (nodes[y].k == K::Add || nodes[y].k == K::Sub)) {
+      const int p = nodes[y].a[0], q = nodes[y].a[1];
+      if (nodes[y].k == K::Add && nodes[q].uniform) return sub(sub(x, q), p);
+      if (nodes[y].k == K::Add && nodes[p].uniform) return sub(sub(x, p), q);
+      if (nodes[y].k == K::Sub && nodes[q].uniform) return sub(add(x, q), p);
+      if (nodes[y].k == K::Sub && nodes[p].uniform) return add(q, sub(x, p));
+    }
     return op(K::Sub, {x, y});
   }
   int mul(int x, int y) {
@@ -372,9 +386,61 @@ struct Dag {
     if (is_num(x) && num(x) == 1.0) return rcp(y);
     return op(K::Div, {x, y});                                   // x * rcp(y) per particle
   }
+  // structural signature of a subtree (stable across the two lowering passes)
+  const std::string& sig(int id) {
+    auto it = sigmemo.find(id);
+    if (it != sigmemo.end()) return it->second;
+    const DNode& n = nodes[id];
+    std::ostringstream o;
+    if (n.k == K::Num) {
+      uint64_t bits;
+      std::memcpy(&bits, &n.value, 8);
+      o << 'n' << bits;
+    } else {
+      o << 'k' << (int)n.k << '.' << n.index << '(';
+      for (int x : n.a) o << sig(x) << ',';
+      o << ')';
+    }
+    return sigmemo[id] = o.str();
+  }
+  // u = c w + d with c, d literal constants and w varying?
+  bool affine(int u, int& w, double& c, double& d) {
+    d = 0.0;
+    const DNode& n = nodes[u];
+    if (n.uniform) return false;
+    int m = u;
+    if (n.k == K::Add && is_num(n.a[1])) { d = num(n.a[1]); m = n.a[0]; }
+    const DNode& nm = nodes[m];
+    if (nm.k == K::Mul && is_num(nm.a[0])) { c = num(nm.a[0]); w = nm.a[1]; }
+    else { c = 1.0; w = m; }
+    return c != 0.0;
+  }
+  int powchain(int b, long r) {
+    if (r == 1) return b;
+    if (r % 2 == 0) { int h = powchain(b, r / 2); return mul(h, h); }
+    return mul(powchain(b, r - 1), b);
+  }
   int exp_(int u) {  // e^u = 2^(log2(e) u)
     if (is_num(u)) return N(std::exp(num(u)));
-    return op(K::Exp2, {mul(N(1.4426950408889634), u)});
+    const int arg = mul(N(1.4426950408889634), u);
+    int w;
+    double c, d;
+    if (affine(arg, w, c, d)) {
+      const std::string& sw = sig(w);
+      exp_uses.push_back({sw, {c, d}});
+      if (plan) {
+        auto it = plan->find(sw);
+        if (it != plan->end()) {
+          const double c0 = it->second, r = c / c0, rr = std::round(r);
+          if (rr >= 1 && rr <= 16 && std::fabs(r - rr) < 1e-9 && std::fabs(d) < 64) {
+            const int base = op(K::Exp2, {mul(N(c0), w)});
+            const int p = powchain(base, (long)rr);
+            return d == 0.0 ? p : mul(N(std::exp2(d)), p);
+          }
+        }
+      }
+    }
+    return op(K::Exp2, {arg});
   }
   int powi(int x, long n) {
     if (n == 0) return N(1.0);
@@ -428,7 +494,20 @@ struct Dag {
         if (f == "pow") return pow_(x, y);
         if (f == "min") return (is_num(x) && is_num(y)) ? N(std::fmin(num(x), num(y))) : op(K::Min, {x, y});
         if (f == "max") return (is_num(x) && is_num(y)) ? N(std::fmax(num(x), num(y))) : op(K::Max, {x, y});
-        if (f == "vtrap") return op(K::Vtrap, {x, y, rcp(y)});
+        if (f == "vtrap") {
+          // x / (exp(x/y) - 1), and for |x/y| < 0.1 the series y (1 - u/2 + u^2/12 - u^4/720)
+          // (reading R10); lowered to primitives so its exponential can be shared (exp_)
+          const int u = mul(x, rcp(y));
+          const int dir = div(x, sub(exp_(u), N(1.0)));
+          const int u2 = mul(u, u);
+          const int ser = mul(y, sub(add(sub(N(1.0), mul(N(0.5), u)), mul(N(1.0 / 12.0), u2)),
+                                     mul(N(1.0 / 720.0), mul(u2, u2))));
+          DNode sn;
+          sn.k = K::SelAbsLt;
+          sn.value = 0.1;
+          sn.a = {u, ser, dir};
+          return intern(sn);
+        }
         throw Error(FF_ERR_PARSE, "internal: unhandled function " + f);
       }
     }
@@ -586,6 +665,7 @@ struct SignSelect {
       case K::Pow: return "ff_pow(" + A(0) + ", " + A(1) + ")";
       case K::Sigmoid2: return "ff_rcp(1.0f + ff_exp2(" + A(0) + "))";
       case K::Vtrap: return "ff_vtrap(" + A(0) + ", " + A(1) + ", " + A(2) + ")";
+      case K::SelAbsLt: return "ff_sel_abs_lt(" + A(0) + ", " + A(1) + ", " + A(2) + ", " + flit(n.value) + ")";
       default: throw Error(FF_ERR_COMPILE, "internal: unexpected node in expr()");
     }
   }
@@ -595,7 +675,10 @@ struct SignSelect {
   // reference to an expression equal to (s ? -v : v)
   std::string get(int id, int s) {
     const DNode& n = g.nodes[id];
-    if (n.uniform) return s ? "(-" + ureference(id) + ")" : ureference(id);
+    if (n.uniform) {
+      if (n.k == K::Num) return flit(s ? -n.value : n.value);
+      return s ? "(-" + ureference(id) + ")" : ureference(id);
+    }
     if (n.k == K::Neg) return get(n.a[0], s ^ 1);
     if (n.k == K::Sweep) return s ? "nsw" : "sw";
     if (n.k == K::Var && s == 0) return "x[" + std::to_string(n.index) + "]";
@@ -639,6 +722,7 @@ struct SignSelect {
       case K::Pow: n_mufu += 2; ++n_arith; break;
       case K::Sigmoid2: n_mufu += 2; ++n_arith; break;
       case K::Vtrap: n_mufu += 2; n_arith += 9; break;
+      case K::SelAbsLt: n_arith += 2; break;
       default: ++n_arith;
     }
   }
@@ -649,7 +733,32 @@ struct SignSelect {
 std::string emit_source(const System& s, int sweep_param) {
   if (sweep_param < -1 || sweep_param >= (int)s.param_names.size())
     throw Error(FF_ERR_INVALID_ARG, "sweep parameter index out of range");
+  // pass 1: lower once to find exponentials sharing an affine argument c w + d
+  std::map<std::string, double> plan;
+  {
+    Dag g1(sweep_param);
+    for (int i = 0; i < s.dim; ++i) g1.lower(s.rhs[i]);
+    std::map<std::string, std::set<std::pair<double, double>>> by_w;
+    for (auto& e : g1.exp_uses) by_w[e.first].insert(e.second);
+    for (auto& kv : by_w) {
+      if (kv.second.size() < 2) continue;
+      double best_c0 = 0;
+      size_t best_n = 0;
+      for (auto& cand : kv.second) {
+        const double c0 = cand.first;
+        size_t n = 0;
+        for (auto& o : kv.second) {
+          const double r = o.first / c0, rr = std::round(r);
+          if (rr >= 1 && rr <= 16 && std::fabs(r - rr) < 1e-9) ++n;
+        }
+        if (n > best_n || (n == best_n && std::fabs(c0) < std::fabs(best_c0))) { best_n = n; best_c0 = c0; }
+      }
+      if (best_n >= 2) plan[kv.first] = best_c0;
+    }
+  }
+  // pass 2: lower with the sharing plan
   Dag g(sweep_param);
+  g.plan = &plan;
   std::vector<int> roots;
   for (int i = 0; i < s.dim; ++i) roots.push_back(g.lower(s.rhs[i]));
 
