@@ -390,7 +390,8 @@ def main():
             "roofline": roof, "clocks": clocks, "gpu_launches": r["launches"], "e2e": r["e2e"],
             "kernel_ms_mean": r["kern_ms"], "frame_ms_p10_p50_p90": [float(np.percentile(r["frame_ms"], q))
                                                                      for q in (10, 50, 90)],
-            "image_sum_last_frame": r["image_sum"], "wall_s_timed_region": r["t_wall"]}
+            "image_sum_last_frame": r["image_sum"], "wall_s_timed_region": r["t_wall"],
+            "build": __import__("paper_1505_00344_b200.fireflies", fromlist=["x"]).ff_build_info()}
     if world == 1 and not args.no_cpu_baseline:
         n = reference_sample_size(w, r["S"])
         v, dt, threads = cpu_oracle_sample(w, n, r["S"])

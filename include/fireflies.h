@@ -87,6 +87,10 @@ const char* ff_last_error(void);
 /* FF_ABI_VERSION of the loaded library. */
 int ff_abi_version(void);
 
+/* Human-readable build information (ABI version, NVRTC version and path, target sm_100a); same
+ * buffer protocol as ff_emit_source. Errors: FF_ERR_COMPILE if NVRTC cannot be loaded. */
+ff_status ff_build_info(char* buf, size_t cap, size_t* len);
+
 /* Front end only (no device needed; "kernel source ... generated automatically"):
  * parse, validate and emit the CUDA C source of the system's kernels. sweep_param = index of the
  * parameter that is per-particle in this variant, or -1. Writes at most cap bytes (NUL-terminated)

@@ -19,7 +19,7 @@ FF_MAX_PARAMS = 128
 FF_MAX_GROUPS = 16
 
 # Every symbol include/fireflies.h declares (checked by tests/test_abi.py).
-EXPORTS = ["ff_last_error", "ff_abi_version", "ff_emit_source", "ff_compile_cubin", "ff_create", "ff_destroy",
+EXPORTS = ["ff_last_error", "ff_abi_version", "ff_build_info", "ff_emit_source", "ff_compile_cubin", "ff_create", "ff_destroy",
            "ff_set_stream", "ff_set_shard", "ff_shard_range", "ff_bind_state", "ff_group_slots", "ff_init_group", "ff_group_info",
            "ff_set_param", "ff_get_param", "ff_sweep_param", "ff_project", "ff_step", "ff_set_launch",
            "ff_read_state", "ff_write_state", "ff_read_image", "ff_launch_count", "ff_sync"]
@@ -54,6 +54,7 @@ def lib():
         sig = {
             "ff_last_error": ([], C.c_char_p),
             "ff_abi_version": ([], C.c_int),
+            "ff_build_info": ([P, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
             "ff_emit_source": ([sysp, i32, P, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
             "ff_compile_cubin": ([sysp, i32, P, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
             "ff_create": ([sysp, i32, C.POINTER(P)], C.c_int),

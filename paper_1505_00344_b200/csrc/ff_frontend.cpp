@@ -18,6 +18,7 @@
 #include <cctype>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -806,9 +807,12 @@ std::string emit_source(const System& s, int sweep_param) {
   rhs << "};\n";
 
   const int dim = s.dim;
-  const int unroll = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
-  const int minb_p1 = dim <= 4 ? 4 : (dim <= 8 ? 3 : (dim <= 16 ? 2 : 1));
-  const int minb_p2 = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
+  int unroll = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
+  int minb_p1 = dim <= 4 ? 4 : (dim <= 8 ? 3 : (dim <= 16 ? 2 : 1));
+  int minb_p2 = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
+  // tuning knobs for experiments (not part of the ABI): FF_TUNE_MINB_P2, FF_TUNE_UNROLL
+  if (const char* e = std::getenv("FF_TUNE_MINB_P2")) minb_p2 = std::atoi(e);
+  if (const char* e = std::getenv("FF_TUNE_UNROLL")) unroll = std::atoi(e);
   std::ostringstream pre;
   pre << "// Fireflies kernels, generated by the libfireflies front end for sm_100a.\n";
   pre << "#define FF_DIM " << dim << "\n";

@@ -57,6 +57,9 @@ std::string emit_source(const System& s, int sweep_param);
 // NVRTC: source -> sm_100a CUBIN (throws Error(FF_ERR_COMPILE) with the log).
 std::vector<char> compile_cubin(const std::string& source, const std::string& name);
 
+// "NVRTC <major>.<minor> (<path>)" of the compiler in use (loads it if needed).
+std::string nvrtc_description();
+
 // The embedded device template text (ff_device.cuh), generated at build time.
 extern const char* const kDeviceTemplate;
 

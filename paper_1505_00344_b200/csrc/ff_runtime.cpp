@@ -227,6 +227,14 @@ const char* ff_last_error(void) { return g_err.c_str(); }
 
 int ff_abi_version(void) { return FF_ABI_VERSION; }
 
+ff_status ff_build_info(char* buf, size_t cap, size_t* len) {
+  FF_TRY
+  std::string info = "libfireflies ABI " + std::to_string(FF_ABI_VERSION) + "; target sm_100a CUBIN; " +
+                     ff::nvrtc_description();
+  return copy_out(info, true, buf, cap, len);
+  FF_CATCH
+}
+
 ff_status ff_emit_source(const ff_system* sys, int sweep_param, char* buf, size_t cap, size_t* len) {
   FF_TRY
   ff::System s = ff::parse_system(sys);

@@ -27,6 +27,12 @@ def ff_abi_version() -> int:
     return lib().ff_abi_version()
 
 
+def ff_build_info() -> str:
+    buf = C.create_string_buffer(1024)
+    check(lib().ff_build_info(buf, 1024, None))
+    return buf.value.decode()
+
+
 def ff_emit_source(system: SystemDef, sweep_param: int = -1) -> str:
     s, keep = make_system(system.var_names, system.rhs, system.params)
     n = C.c_size_t(0)
