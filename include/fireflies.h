@@ -194,6 +194,22 @@ ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view
  * Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE (no groups), FF_ERR_CUDA. */
 ff_status ff_step(ff_ctx* ctx, int64_t n_steps, float dt);
 
+/* Device-side reset (trajectories that leave the region, or have not been reset for
+ * more than T_max, get new random initial conditions; per-variable bounds; the paper
+ * does this on the host, lagged). When enabled, every ff_step with n_steps > 0 checks
+ * each particle after its last step, before binning: it is reset if a component is non-finite, or
+ * (lo/hi given) outside [lo_d, hi_d], or (t_max > 0 and finite) its simulated time since the last
+ * (re)initialisation exceeds t_max. A reset particle gets the group's IC formula (reading R5) with
+ * Philox stream 2 + e, e = number of earlier resets of that particle; its swept value is unchanged.
+ * lo, hi: HOST arrays of dim floats (both or neither). enable = 0 disables (bookkeeping kept).
+ * Allocates library-owned device memory (8 bytes per slot). Call after ff_bind_state; groups created
+ * before or after are covered. Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE, FF_ERR_CUDA. */
+ff_status ff_set_reset(ff_ctx* ctx, int enable, const float* lo, const float* hi, float t_max);
+
+/* Reset counts (epochs) of particles [first, first+count) of a group into a HOST uint32 buffer
+ * (synchronous). Errors: FF_ERR_STATE (reset never enabled), FF_ERR_INVALID_ARG. */
+ff_status ff_read_epochs(ff_ctx* ctx, int group_id, int64_t first, int64_t count, uint32_t* host);
+
 /* Kernel selection: particles per thread (1 or 2; 2 packs pairs into FFMA2) and threads per
  * block (128, 256 or 512); 0 = library default. For tuning/benchmarks. */
 ff_status ff_set_launch(ff_ctx* ctx, int particles_per_thread, int threads_per_block);

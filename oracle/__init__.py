@@ -162,3 +162,26 @@ def histogram(x_soa, axes, view, W: int, H: int, C_: int, colour: int, image=Non
     if rc != 0:
         raise ValueError("orc_histogram_f32 rejected its arguments")
     return image
+
+
+def reset(x_soa, bound_lo, bound_hi, t_max, t_now, birth, epoch, ic_lo, ic_hi, seed, first_global=0):
+    """Apply the reset rule (fireflies_oracle.c) in place to float32 x_soa (dim, n),
+    float32 birth (n) and uint32 epoch (n). bound_lo/hi None = non-finite check only."""
+    L = lib()
+    if not hasattr(L, "_reset_sig"):
+        L.orc_reset_f32.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_float,
+                                    C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int64]
+        L.orc_reset_f32.restype = C.c_int
+        L._reset_sig = True
+    assert x_soa.dtype == np.float32 and x_soa.flags.c_contiguous
+    assert birth.dtype == np.float32 and epoch.dtype == np.uint32
+    dim, n = x_soa.shape
+    blo = None if bound_lo is None else np.ascontiguousarray(bound_lo, dtype=np.float32)
+    bhi = None if bound_hi is None else np.ascontiguousarray(bound_hi, dtype=np.float32)
+    lo = np.ascontiguousarray(ic_lo, dtype=np.float32)
+    hi = np.ascontiguousarray(ic_hi, dtype=np.float32)
+    rc = L.orc_reset_f32(_ptr(x_soa), n, n, dim, _ptr(blo), _ptr(bhi), t_max, t_now, _ptr(birth), _ptr(epoch),
+                         _ptr(lo), _ptr(hi), seed, first_global)
+    if rc != 0:
+        raise ValueError("orc_reset_f32 rejected its arguments")
+    return x_soa

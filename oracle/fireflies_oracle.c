@@ -257,4 +257,45 @@ int orc_histogram_f32(const float* x_soa, int64_t n, int64_t pitch, int dim, con
   return 0;
 }
 
+/* =====================================================================================
+ * Reset ("Any trajectories that leave this square region, or which have not been
+ * reset for more than time T_max, are reset to a new random set of initial conditions";
+ * per-variable bounds; reading R16). Applied to particles
+ * first_global .. first_global + n - 1 of one group (SoA x[d*pitch + j]):
+ *   bad = (bounds given ? some component outside [lo_d, hi_d] (NaN counts as outside)
+ *                       : some component non-finite)
+ *         or (age on: (t_now - birth[j]) > t_max)      (t_max > 0 and finite = age on)
+ *   if bad: e = epoch[j]; epoch[j] = e + 1; birth[j] = t_now;
+ *           x_d = uniform_in_box(ic_lo_d, ic_hi_d, u) with u from Philox word d%4 of
+ *                 ctr {i lo, i hi, d/4, 2 + e}, key = seed   (stream 2 + e; reading R5)
+ * ===================================================================================== */
+int orc_reset_f32(float* x, int64_t n, int64_t pitch, int dim, const float* bound_lo, const float* bound_hi,
+                  float t_max, float t_now, float* birth, uint32_t* epoch, const float* ic_lo, const float* ic_hi,
+                  uint64_t seed, int64_t first_global) {
+  if (dim < 1 || n < 0 || pitch < n || (bound_lo == NULL) != (bound_hi == NULL)) return -1;
+  const int age_on = t_max > 0.0f && isfinite(t_max);
+  for (int64_t j = 0; j < n; ++j) {
+    int bad = 0;
+    for (int d = 0; d < dim; ++d) {
+      const float v = x[(int64_t)d * pitch + j];
+      if (bound_lo) {
+        if (!(v >= bound_lo[d] && v <= bound_hi[d])) bad = 1;
+      } else {
+        if (!isfinite(v)) bad = 1;
+      }
+    }
+    if (age_on && (t_now - birth[j]) > t_max) bad = 1;
+    if (!bad) continue;
+    const uint32_t e = epoch[j];
+    epoch[j] = e + 1u;
+    birth[j] = t_now;
+    const uint64_t i = (uint64_t)(first_global + j);
+    for (int d = 0; d < dim; ++d) {
+      const uint32_t r = philox_word(seed, i, (uint32_t)(d / 4), 2u + e, d % 4);
+      x[(int64_t)d * pitch + j] = uniform_in_box(ic_lo[d], ic_hi[d], u01_from_word(r));
+    }
+  }
+  return 0;
+}
+
 int orc_version(void) { return 1; }

@@ -21,7 +21,8 @@ FF_MAX_GROUPS = 16
 # Every symbol include/fireflies.h declares (checked by tests/test_abi.py).
 EXPORTS = ["ff_last_error", "ff_abi_version", "ff_build_info", "ff_emit_source", "ff_compile_cubin", "ff_create", "ff_destroy",
            "ff_set_stream", "ff_set_shard", "ff_shard_range", "ff_bind_state", "ff_group_slots", "ff_init_group", "ff_group_info",
-           "ff_set_param", "ff_get_param", "ff_sweep_param", "ff_project", "ff_step", "ff_set_launch",
+           "ff_set_param", "ff_get_param", "ff_sweep_param", "ff_project", "ff_step", "ff_set_reset",
+           "ff_read_epochs", "ff_set_launch",
            "ff_read_state", "ff_write_state", "ff_read_image", "ff_launch_count", "ff_sync"]
 
 
@@ -71,6 +72,8 @@ def lib():
             "ff_sweep_param": ([P, i32, C.c_char_p, f32, f32, i32, u64], C.c_int),
             "ff_project": ([P, P, i32, P, i32, i32, i32, P], C.c_int),
             "ff_step": ([P, i64, f32], C.c_int),
+            "ff_set_reset": ([P, i32, P, P, f32], C.c_int),
+            "ff_read_epochs": ([P, i32, i64, i64, P], C.c_int),
             "ff_set_launch": ([P, i32, i32], C.c_int),
             "ff_read_state": ([P, i32, i64, i64, P], C.c_int),
             "ff_write_state": ([P, i32, i64, i64, P], C.c_int),

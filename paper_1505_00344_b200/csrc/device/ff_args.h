@@ -13,6 +13,7 @@ typedef long long ff_i64;
 typedef unsigned int ff_u32;
 
 #define FF_MAX_GROUPS_ 16
+#define FF_MAX_DIM_ 64
 #ifndef FF_NP_ALLOC
 #define FF_NP_ALLOC 128  /* host side: FF_MAX_PARAMS; device side: the system's count */
 #endif
@@ -28,6 +29,9 @@ struct FFGroup {
   float sw_lo, sw_hi, sw_top, sw_val;  // sweep range, largest float below hi, uniform value
   int sweep_mode;       // -1: every particle uses sw_val; 0: Philox-uniform; 1: linspace
   int colour;           // image channel
+  ff_u64 seed;          // IC seed of the group (resets draw from it with stream 2 + epoch)
+  float t_now;          // simulated time elapsed in this group after this launch (for T_max)
+  int pad_;
 };
 
 struct FFStepArgs {
@@ -42,6 +46,13 @@ struct FFStepArgs {
   float view[16];
   float s0, s1;         // 2-D scales W/(hi0-lo0), H/(hi1-lo1), computed by the host in float
   int n_groups;
+  // device-side reset (NEXT row 1): 0 off, else bit 1 = bounds, bit 2 = age
+  int reset;
+  float t_max;
+  ff_u32* epoch;        // per slot: resets so far (library-owned)
+  float* birth;         // per slot: group time of the last (re)initialisation (library-owned)
+  const float* ic_box;  // [group][lo | hi | top][dim] (library-owned)
+  float bound_lo[FF_MAX_DIM_], bound_hi[FF_MAX_DIM_];
   FFGroup g[FF_MAX_GROUPS_];
   float p[FF_NP_ALLOC]; // parameter values (must stay the last member)
 };

@@ -17,8 +17,9 @@
 #include "device/ff_args.h"
 #include "ff_internal.hpp"
 
-static_assert(sizeof(FFGroup) == 88, "FFGroup layout");
-static_assert(offsetof(FFStepArgs, g) == 144, "FFStepArgs layout");
+static_assert(sizeof(FFGroup) == 104, "FFGroup layout");
+static_assert(offsetof(FFStepArgs, g) == 688, "FFStepArgs layout");
+static_assert(FF_MAX_DIM_ == FF_MAX_DIM, "bounds table size");
 static_assert(FF_MAX_GROUPS_ == FF_MAX_GROUPS, "group table size");
 
 namespace {
@@ -85,10 +86,51 @@ struct ff_ctx {
   float s0 = 0, s1 = 0;
   int ppt = 0, tpb = 0;
   int64_t launches = 0;
+  // device-side reset (ff_set_reset): library-owned per-slot epoch / birth time, IC boxes
+  int reset = 0;
+  float t_max = 0.0f;
+  std::vector<float> bound_lo, bound_hi;
+  uint32_t* epoch = nullptr;
+  float* birth = nullptr;
+  float* ic_box = nullptr;
+  std::vector<double> t_elapsed;  // per group: simulated time since creation (sum of |dt| n)
 
   ~ff_ctx() {
     for (auto& m : modules)
       if (m.second.lib) cudaLibraryUnload(m.second.lib);
+    free_reset_buffers();
+  }
+
+  void free_reset_buffers() {
+    if (epoch) cudaFree(epoch);
+    if (birth) cudaFree(birth);
+    if (ic_box) cudaFree(ic_box);
+    epoch = nullptr;
+    birth = nullptr;
+    ic_box = nullptr;
+  }
+
+  // (re)initialise the reset bookkeeping of group gi: epoch 0, birth = current group time, IC box
+  void reset_init_group(size_t gi) {
+    if (!reset) return;
+    const GroupRec& G = groups[gi];
+    const int dim = sys.dim;
+    const size_t n = (size_t)(G.slot_end - G.slot_begin);
+    if (n) {
+      ck(cudaMemsetAsync(epoch + G.slot_begin, 0, n * sizeof(uint32_t), stream), "cudaMemsetAsync epoch");
+      std::vector<float> b(n, (float)t_elapsed[gi]);
+      ck(cudaMemcpyAsync(birth + G.slot_begin, b.data(), n * sizeof(float), cudaMemcpyHostToDevice, stream),
+         "cudaMemcpyAsync birth");
+    }
+    std::vector<float> box(3 * (size_t)dim);
+    for (int d = 0; d < dim; ++d) {
+      box[d] = G.lo[d];
+      box[dim + d] = G.hi[d];
+      box[2 * dim + d] = std::nextafter(G.hi[d], -INFINITY);
+    }
+    ck(cudaMemcpyAsync(ic_box + gi * 3 * (size_t)dim, box.data(), box.size() * sizeof(float), cudaMemcpyHostToDevice,
+                       stream), "cudaMemcpyAsync ic_box");
+    ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize");  // host buffers go out of scope
   }
 
   Module& module(int sweep) {
@@ -151,9 +193,21 @@ struct ff_ctx {
     a.s0 = s0;
     a.s1 = s1;
     a.n_groups = (int)groups.size();
+    a.reset = n_steps > 0 ? reset : 0;
+    a.t_max = t_max;
+    a.epoch = epoch;
+    a.birth = birth;
+    a.ic_box = ic_box;
+    for (size_t d = 0; d < bound_lo.size(); ++d) {
+      a.bound_lo[d] = bound_lo[d];
+      a.bound_hi[d] = bound_hi[d];
+    }
     for (size_t gi = 0; gi < groups.size(); ++gi) {
       const GroupRec& G = groups[gi];
       FFGroup& g = a.g[gi];
+      t_elapsed[gi] += std::fabs((double)dt) * (double)n_steps;
+      g.seed = G.seed;
+      g.t_now = (float)t_elapsed[gi];
       g.slot_begin = G.slot_begin;
       g.slot_end = G.slot_end;
       g.n_local = G.n_local;
@@ -311,6 +365,9 @@ ff_status ff_bind_state(ff_ctx* ctx, float* dev_state, int64_t pitch, int64_t ca
   ctx->capacity = capacity;
   ctx->next_slot = 0;
   ctx->groups.clear();
+  ctx->t_elapsed.clear();
+  ctx->reset = 0;
+  ctx->free_reset_buffers();
   FF_CATCH
 }
 
@@ -383,7 +440,57 @@ ff_status ff_init_group(ff_ctx* ctx, const float* ic_lo, const float* ic_hi, int
   }
   ctx->next_slot = g.slot_end;
   ctx->groups.push_back(g);
+  ctx->t_elapsed.push_back(0.0);
+  ctx->reset_init_group(ctx->groups.size() - 1);
   if (group_id) *group_id = (int)ctx->groups.size() - 1;
+  FF_CATCH
+}
+
+ff_status ff_set_reset(ff_ctx* ctx, int enable, const float* lo, const float* hi, float t_max) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  if (!enable) {
+    ctx->reset = 0;
+    return FF_OK;
+  }
+  need(ctx->state != nullptr, FF_ERR_STATE, "no state bound (ff_bind_state)");
+  need((lo == nullptr) == (hi == nullptr), FF_ERR_INVALID_ARG, "give both bounds or neither");
+  const int dim = ctx->sys.dim;
+  std::vector<float> blo, bhi;
+  if (lo) {
+    for (int d = 0; d < dim; ++d) {
+      need(!std::isnan(lo[d]) && !std::isnan(hi[d]) && lo[d] <= hi[d], FF_ERR_INVALID_ARG, "bounds need lo <= hi");
+      blo.push_back(lo[d]);
+      bhi.push_back(hi[d]);
+    }
+  }
+  need(!std::isnan(t_max), FF_ERR_INVALID_ARG, "t_max is NaN");
+  ctx->free_reset_buffers();
+  const size_t cap = (size_t)ctx->pitch;
+  ck(cudaMalloc(&ctx->epoch, cap * sizeof(uint32_t)), "cudaMalloc epoch");
+  ck(cudaMalloc(&ctx->birth, cap * sizeof(float)), "cudaMalloc birth");
+  ck(cudaMalloc(&ctx->ic_box, (size_t)FF_MAX_GROUPS * 3 * dim * sizeof(float)), "cudaMalloc ic_box");
+  ctx->bound_lo = blo;
+  ctx->bound_hi = bhi;
+  ctx->t_max = t_max;
+  ctx->reset = (lo ? 1 : 0) | ((t_max > 0.0f && std::isfinite(t_max)) ? 2 : 0);
+  if (!ctx->reset) ctx->reset = 4;  // non-finite check only
+  for (size_t gi = 0; gi < ctx->groups.size(); ++gi) ctx->reset_init_group(gi);
+  FF_CATCH
+}
+
+ff_status ff_read_epochs(ff_ctx* ctx, int group_id, int64_t first, int64_t count, uint32_t* host) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  need(ctx->reset && ctx->epoch, FF_ERR_STATE, "reset is not enabled");
+  const GroupRec& g = ctx->group(group_id);
+  need(host || count == 0, FF_ERR_INVALID_ARG, "host buffer is NULL");
+  need(first >= 0 && count >= 0 && first + count <= g.n_local, FF_ERR_INVALID_ARG, "particle range out of bounds");
+  if (count) {
+    ck(cudaMemcpyAsync(host, ctx->epoch + g.slot_begin + first, (size_t)count * sizeof(uint32_t),
+                       cudaMemcpyDeviceToHost, ctx->stream), "cudaMemcpyAsync epochs");
+    ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+  }
   FF_CATCH
 }
 

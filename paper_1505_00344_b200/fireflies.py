@@ -125,6 +125,19 @@ def ff_step(ctx, n_steps: int, dt: float):
     check(lib().ff_step(ctx, n_steps, dt))
 
 
+def ff_set_reset(ctx, enable: bool, lo=None, hi=None, t_max: float = 0.0):
+    lo_a = None if lo is None else np.ascontiguousarray(lo, dtype=np.float32)
+    hi_a = None if hi is None else np.ascontiguousarray(hi, dtype=np.float32)
+    check(lib().ff_set_reset(ctx, 1 if enable else 0, None if lo_a is None else _fptr(lo_a),
+                             None if hi_a is None else _fptr(hi_a), t_max))
+
+
+def ff_read_epochs(ctx, group_id: int, first: int, count: int) -> np.ndarray:
+    out = np.empty(count, dtype=np.uint32)
+    check(lib().ff_read_epochs(ctx, group_id, first, count, _fptr(out)))
+    return out
+
+
 def ff_set_launch(ctx, particles_per_thread: int = 0, threads_per_block: int = 0):
     check(lib().ff_set_launch(ctx, particles_per_thread, threads_per_block))
 
@@ -230,6 +243,14 @@ class Context:
 
     def step(self, n_steps, dt):
         ff_step(self.ctx, n_steps, dt)
+
+    def set_reset(self, enable=True, lo=None, hi=None, t_max=0.0):
+        ff_set_reset(self.ctx, enable, lo, hi, t_max)
+
+    def read_epochs(self, g, first=0, count=None):
+        _, n, _ = ff_group_info(self.ctx, g)
+        count = n - first if count is None else count
+        return ff_read_epochs(self.ctx, g, first, count)
 
     def set_launch(self, ppt=0, tpb=0):
         ff_set_launch(self.ctx, ppt, tpb)
