@@ -55,6 +55,12 @@ WORKLOADS = {
                                box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj="lorenz_camera", W=1024, H=1024,
                                C=2, S=100, dt=0.01, fma_ops=45, mufu_ops=0, bound="alu", prerun=4000,
                                desc="Lorenz r=0.5 after 4000 steps: 8M particles in ~1 pixel (histogram stress)"),
+    "stn_bif3d": dict(system="stn_gpe", groups=[(1 << 22, 1, 0, 21), (1 << 22, -1, 1, 22)], params={},
+                      sweep=("w_ss", 0.0, 12.0, 0, 23), reset=([0.0, 0.0], [1.0, 1.0], 0.0),
+                      box=([0.0, 0.0], [1.0, 1.0]), proj="stn_box_camera", W=1024, H=1024, C=2, S=100, dt=0.01,
+                      fma_ops=None, mufu_ops=16, bound="xu",
+                      desc="STN-GPe 3-D bifurcation (x, y, w_ss in [0,12)), 4M fwd + 4M bwd with reset "
+                           "(PAPER.md:54, :59; NEXT row 4)"),
     "lorenz1b": dict(system="lorenz", groups=[(1 << 30, 1, 0, 6)], params={"r": 28.0}, strong=True,
                      box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj="lorenz_camera", W=1024, H=1024, C=1,
                      S=100, dt=0.01, fma_ops=45, mufu_ops=0, bound="alu",
@@ -123,6 +129,8 @@ def projection(w):
     from paper_1505_00344_b200 import views
     if w["proj"] == "lorenz_camera":
         return [0, 1, 2], views.lorenz_camera()
+    if w["proj"] == "stn_box_camera":
+        return [0, 1, 2], views.box_camera([0.0, 0.0, 0.0], [1.0, 1.0, 12.0])
     return w["proj"]
 
 
@@ -146,6 +154,8 @@ def run_ours(args, w, rank, world, device):
         name, a, b, mode, seed = w["sweep"]
         for g in gids:
             ctx.sweep_param(g, name, a, b, mode, seed)
+    if "reset" in w:
+        ctx.set_reset(True, *w["reset"])
     if w.get("prerun"):
         ctx.step(w["prerun"], w["dt"])
     axes, view = projection(w)

@@ -40,3 +40,17 @@ def view_projection(eye, target, up, fov_y_deg=45.0, aspect=1.0, near=1.0, far=5
 def lorenz_camera():
     """Config-2 camera: eye (0,-120,25) looking at (0,0,25), up +z, fov 45."""
     return view_projection((0.0, -120.0, 25.0), (0.0, 0.0, 25.0), (0.0, 0.0, 1.0))
+
+
+def box_camera(lo, hi, eye_dir=(1.6, -2.2, 1.2), fov_y_deg=40.0, aspect=1.0):
+    """View-projection that first maps the axis box [lo, hi] (3 axes, possibly of very different
+    extents, e.g. (x, y, w_ss) of the STN-GPe bifurcation diagram) onto the unit
+    cube centred at the origin, then looks at it from direction `eye_dir` (row-major float32)."""
+    lo, hi = np.asarray(lo, np.float64), np.asarray(hi, np.float64)
+    S = np.eye(4)
+    S[:3, :3] = np.diag(1.0 / (hi - lo))
+    S[:3, 3] = -(lo + hi) / 2 / (hi - lo)
+    d = np.asarray(eye_dir, np.float64)
+    eye = d / np.linalg.norm(d) * 2.6
+    P = perspective(fov_y_deg, aspect, 0.1, 20.0) @ look_at(eye, (0.0, 0.0, 0.0), (0.0, 0.0, 1.0))
+    return (P @ S).astype(np.float32)

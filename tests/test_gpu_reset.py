@@ -93,6 +93,41 @@ def test_age_reset_all_particles():
     assert np.array_equal(ctx.read_state(g).view(np.uint32), x.view(np.uint32))
 
 
+def test_stn_bifurcation_3d_pipeline():
+    # NEXT row 4: w_ss lifted (swept per particle over [0, 12)), forward and
+    # backward groups, reset to the unit square, 3-D projection of (x, y, w_ss). One fused launch of
+    # 100 steps + reset + binning, checked against oracle integration + reset + histogram.
+    s, p = stn_params()
+    n = 6000 + 7
+    ctx = FF.Context(s, [n, n])
+    gf = ctx.init_group([0, 0], [1, 1], n, 1, 0, seed=21)
+    gb = ctx.init_group([0, 0], [1, 1], n, -1, 1, seed=22)
+    for g in (gf, gb):
+        ctx.sweep_param(g, "w_ss", 0.0, 12.0, 0, 23)
+    ctx.set_reset(True, [0.0, 0.0], [1.0, 1.0], 0.0)
+    M = views.box_camera([0.0, 0.0, 0.0], [1.0, 1.0, 12.0])
+    img = ctx.project([0, 1, 2], M, 256, 256, 2)
+    img.zero_()
+    ctx.step(100, 0.01)
+    sv = O.sweep_values(0.0, 12.0, 0, 23, 0, n, n)
+    want_img = np.zeros((2, 256, 256), np.uint32)
+    t = np.float32(abs(float(np.float32(0.01))) * 100)
+    for g, seed, h, ch in ((gf, 21, 0.01, 0), (gb, 22, -0.01, 1)):
+        x = O.rk4(O.STN, O.ic_uniform([0, 0], [1, 1], seed, 0, n), p, np.float32(h), 100, 0, sv)
+        b, e = np.zeros(n, np.float32), np.zeros(n, np.uint32)
+        O.reset(x, [0, 0], [1, 1], 0.0, t, b, e, [0, 0], [1, 1], seed)
+        got, ge = ctx.read_state(g), ctx.read_epochs(g)
+        same = ge == e
+        assert (~same).sum() <= 3
+        err = scaled_error(got[:, same], x[:, same], [1.0, 1.0])
+        assert err.max() <= 1e-5
+        O.histogram(x, [0, 1, 2], M, 256, 256, 2, ch, image=want_img, sweep_vals=sv)
+    got_img = ctx.read_image().astype(np.int64)
+    # particles near a pixel edge (or with a different reset decision) may land one bin apart
+    assert np.abs(got_img - want_img.astype(np.int64)).sum() <= 2 * 40
+    assert got_img.sum() == want_img.sum()
+
+
 def test_reset_then_binning_sees_new_positions():
     # the fused binning runs after the reset: every particle of a collapsed backward group counts
     s, p = stn_params()
