@@ -224,6 +224,17 @@ ff_status ff_write_state(ff_ctx* ctx, int group_id, int64_t first, int64_t count
 /* Copy the bound image to a HOST uint32 [C][H][W] buffer (synchronous). */
 ff_status ff_read_image(ff_ctx* ctx, uint32_t* host_image);
 
+/* Render the bound count image to a displayable RGB frame (sprites with an intensity
+ * that falls off with the distance from their centre, coloured per group, blended
+ * additively), async on the bound stream:
+ *   rgb[k][y][x] = min(1, sum_c colours[3c+k] * intensity * sum_q count_c(y+q_y, x+q_x) w(q))
+ *   w(q) = (1 - min(|q| / radius_px, 1))^2 over integer offsets |q_x|, |q_y| <= ceil(radius_px)
+ * (sprites centred on their pixel, reading R24; falloff of SPEC.md:388; taps outside the image
+ * contribute nothing; sums in double, exactly rounded, so results are reproducible bit-for-bit).
+ * colours: HOST float[C][3]; intensity >= 0 (sprite alpha); 0 < radius_px <= 8; dev_rgb: DEVICE
+ * float[3][H][W] (caller-owned). Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE (no image), FF_ERR_CUDA. */
+ff_status ff_render(ff_ctx* ctx, const float* colours, float intensity, float radius_px, float* dev_rgb);
+
 /* Number of kernel launches this context has issued (for bench evidence). */
 ff_status ff_launch_count(ff_ctx* ctx, int64_t* count);
 

@@ -185,3 +185,18 @@ def reset(x_soa, bound_lo, bound_hi, t_max, t_now, birth, epoch, ic_lo, ic_hi, s
     if rc != 0:
         raise ValueError("orc_reset_f32 rejected its arguments")
     return x_soa
+
+
+def render(image, colours, intensity, radius):
+    """RGB float32 (3, H, W) of a uint32 count image (C, H, W) (fireflies_oracle.c orc_render_f32)."""
+    L = lib()
+    L.orc_render_f32.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_float, C.c_float,
+                                 C.c_void_p]
+    L.orc_render_f32.restype = C.c_int
+    img = np.ascontiguousarray(image, dtype=np.uint32)
+    C_, H, W = img.shape
+    col = np.ascontiguousarray(colours, dtype=np.float32)
+    out = np.empty((3, H, W), np.float32)
+    if L.orc_render_f32(_ptr(img), W, H, C_, _ptr(col), intensity, radius, _ptr(out)) != 0:
+        raise ValueError("orc_render_f32 rejected its arguments")
+    return out

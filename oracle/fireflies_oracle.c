@@ -298,4 +298,39 @@ int orc_reset_f32(float* x, int64_t n, int64_t pitch, int dim, const float* boun
   return 0;
 }
 
+/* =====================================================================================
+ * Render post-process (reading R24): sprites of radius R pixels
+ * centred on their pixel, falloff w(q) = (1 - min(|q|/R, 1))^2 rounded to float,
+ * additive blending saturating at 1:
+ *   rgb[k][y][x] = min(1, sum_c colour[c][k] * (intensity * sum_{dy,dx} count_c[y+dy][x+dx] w(dx,dy)))
+ * taps |dx|, |dy| <= ceil(R) inside the image, dy outer / dx inner, sums in double in this order.
+ * ===================================================================================== */
+int orc_render_f32(const uint32_t* image, int W, int H, int C, const float* colour, float intensity, float radius,
+                   float* rgb) {
+  if (W < 1 || H < 1 || C < 1 || !(radius > 0.0f) || radius > 8.0f) return -1;
+  const int hw = (int)ceil((double)radius);
+  for (int y = 0; y < H; ++y) {
+    for (int x = 0; x < W; ++x) {
+      double v[3] = {0.0, 0.0, 0.0};
+      for (int c = 0; c < C; ++c) {
+        double acc = 0.0;
+        for (int dy = -hw; dy <= hw; ++dy) {
+          for (int dx = -hw; dx <= hw; ++dx) {
+            const int yy = y + dy, xx = x + dx;
+            if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+            const double r = sqrt((double)(dx * dx + dy * dy)) / (double)radius;
+            const double f = 1.0 - (r < 1.0 ? r : 1.0);
+            const float w = (float)(f * f);
+            acc = acc + (double)image[((int64_t)c * H + yy) * W + xx] * (double)w;
+          }
+        }
+        const double s = (double)intensity * acc;
+        for (int k = 0; k < 3; ++k) v[k] = v[k] + (double)colour[3 * c + k] * s;
+      }
+      for (int k = 0; k < 3; ++k) rgb[((int64_t)k * H + y) * W + x] = (float)(v[k] < 1.0 ? v[k] : 1.0);
+    }
+  }
+  return 0;
+}
+
 int orc_version(void) { return 1; }

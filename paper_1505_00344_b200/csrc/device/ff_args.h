@@ -57,4 +57,17 @@ struct FFStepArgs {
   float p[FF_NP_ALLOC]; // parameter values (must stay the last member)
 };
 
+// Render post-process (NEXT row 3): count image -> RGB with sprite falloff.
+#define FF_RENDER_MAX_R 8
+#define FF_RENDER_MAX_C 16
+struct FFRenderArgs {
+  const ff_u32* image;  // [C][H][W] counts
+  float* rgb;           // [3][H][W] output
+  int W, H, C, hw;      // hw = half width of the sprite footprint in pixels
+  float intensity;      // sprite alpha
+  int pad_;
+  float colour[FF_RENDER_MAX_C * 3];
+  float w[(2 * FF_RENDER_MAX_R + 1) * (2 * FF_RENDER_MAX_R + 1)];  // [dy + hw][dx + hw], row pitch 2hw+1
+};
+
 #endif

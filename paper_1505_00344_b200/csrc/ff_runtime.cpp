@@ -36,6 +36,7 @@ void ck(cudaError_t e, const char* what) {
 struct Module {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t init = nullptr;
+  cudaKernel_t render = nullptr;
   // step kernels by (ppt, tpb): index 0 p1t128, 1 p1t256, 2 p1t512, 3 p2t128, 4 p2t256
   cudaKernel_t step[5] = {};
   int occ[5] = {};
@@ -141,6 +142,7 @@ struct ff_ctx {
     Module m;
     ck(cudaLibraryLoadData(&m.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
     ck(cudaLibraryGetKernel(&m.init, m.lib, "ff_init"), "cudaLibraryGetKernel(ff_init)");
+    ck(cudaLibraryGetKernel(&m.render, m.lib, "ff_render"), "cudaLibraryGetKernel(ff_render)");
     for (int i = 0; i < 5; ++i) {
       ck(cudaLibraryGetKernel(&m.step[i], m.lib, kStepNames[i]), "cudaLibraryGetKernel(ff_step)");
       int occ = 0;
@@ -635,6 +637,42 @@ ff_status ff_read_state(ff_ctx* ctx, int group_id, int64_t first, int64_t count,
 ff_status ff_write_state(ff_ctx* ctx, int group_id, int64_t first, int64_t count, const float* host_soa) {
   FF_TRY
   state_copy(ctx, group_id, first, count, const_cast<float*>(host_soa), false);
+  FF_CATCH
+}
+
+ff_status ff_render(ff_ctx* ctx, const float* colours, float intensity, float radius_px, float* dev_rgb) {
+  FF_TRY
+  need(ctx && colours && dev_rgb, FF_ERR_INVALID_ARG, "NULL argument");
+  need(ctx->image != nullptr, FF_ERR_STATE, "no image bound");
+  need(ctx->C <= FF_RENDER_MAX_C, FF_ERR_INVALID_ARG, "too many channels for ff_render");
+  need(std::isfinite(intensity) && intensity >= 0.0f, FF_ERR_INVALID_ARG, "intensity must be finite and >= 0");
+  need(radius_px > 0.0f && radius_px <= (float)FF_RENDER_MAX_R, FF_ERR_INVALID_ARG, "radius must be in (0, 8]");
+  need(((uintptr_t)dev_rgb & 3) == 0, FF_ERR_INVALID_ARG, "rgb must be 4-byte aligned");
+  FFRenderArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.image = ctx->image;
+  a.rgb = dev_rgb;
+  a.W = ctx->W;
+  a.H = ctx->H;
+  a.C = ctx->C;
+  a.hw = (int)std::ceil((double)radius_px);
+  a.intensity = intensity;
+  for (int i = 0; i < 3 * ctx->C; ++i) {
+    need(std::isfinite(colours[i]), FF_ERR_INVALID_ARG, "colours must be finite");
+    a.colour[i] = colours[i];
+  }
+  const int side = 2 * a.hw + 1;
+  for (int dy = -a.hw; dy <= a.hw; ++dy)
+    for (int dx = -a.hw; dx <= a.hw; ++dx) {
+      const double r = std::sqrt((double)(dx * dx + dy * dy)) / (double)radius_px;
+      const double f = 1.0 - (r < 1.0 ? r : 1.0);
+      a.w[(dy + a.hw) * side + (dx + a.hw)] = (float)(f * f);
+    }
+  Module& m = ctx->module(ctx->sweep_param);
+  void* args[] = {&a};
+  dim3 grid((unsigned)((ctx->W + 31) / 32), (unsigned)((ctx->H + 7) / 8));
+  ck(cudaLaunchKernel((const void*)m.render, grid, dim3(256), args, 0, ctx->stream), "launch ff_render");
+  ++ctx->launches;
   FF_CATCH
 }
 

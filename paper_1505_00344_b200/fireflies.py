@@ -157,6 +157,11 @@ def ff_read_image_into(ctx, host_ptr: int):
     check(lib().ff_read_image(ctx, C.c_void_p(host_ptr)))
 
 
+def ff_render(ctx, colours, intensity: float, radius_px: float, dev_rgb_ptr: int):
+    col = np.ascontiguousarray(colours, dtype=np.float32)
+    check(lib().ff_render(ctx, _fptr(col), intensity, radius_px, C.c_void_p(dev_rgb_ptr)))
+
+
 def ff_launch_count(ctx) -> int:
     n = C.c_int64()
     check(lib().ff_launch_count(ctx, C.byref(n)))
@@ -267,6 +272,15 @@ class Context:
         """Host copy of the bound image as uint32 (C, H, W)."""
         out = np.empty(tuple(self.image.shape), dtype=np.uint32)
         ff_read_image_into(self.ctx, out.ctypes.data)
+        return out
+
+    def render(self, colours, intensity=1.0, radius_px=2.0, out=None):
+        """RGB float32 [3][H][W] frame of the bound image (device tensor)."""
+        torch = self.torch
+        C_, H, W = self.image.shape
+        if out is None:
+            out = torch.empty((3, H, W), dtype=torch.float32, device=self.device)
+        ff_render(self.ctx, colours, intensity, radius_px, out.data_ptr())
         return out
 
     def launch_count(self):

@@ -92,9 +92,10 @@ def test_config4_sweep_16M_rho_y_image():
     y = ctx.group_view(g)[1].cpu().numpy()
     inside = int(((y >= -160) & (y < 160)).sum())           # r is always inside [0, 200)
     assert im.sum() == inside
-    # the r = column histogram: each of the 2048 columns holds ~n/2048 particles (uniform r)
-    col = im[0].sum(axis=0)
-    assert abs(col.mean() - n / 2048) < 1 and col.min() > 0.9 * n / 2048
+    # the r columns: r is uniform in [0, 200), and for r < 50 every particle is still inside the y
+    # window after 10 steps, so each of the first 512 columns holds ~n/2048 particles
+    col = im[0].sum(axis=0)[:512]
+    assert abs(col.mean() - n / 2048) < 20 and col.min() > 0.9 * n / 2048
 
 
 def test_config3_hh_1M():
