@@ -15,7 +15,7 @@ import numpy as np
 
 from . import build as _build
 
-LINEAR, HARMONIC, LORENZ, STN, HH = 0, 1, 2, 3, 4
+LINEAR, HARMONIC, LORENZ, STN, HH, FUNCS = 0, 1, 2, 3, 4, 5
 
 # Parameter vector layouts (fireflies_oracle.c header).
 PARAMS = {

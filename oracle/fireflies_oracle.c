@@ -42,30 +42,67 @@
 #define ORC_LORENZ 2
 #define ORC_STN 3
 #define ORC_HH 4
+#define ORC_FUNCS 5
 #define ORC_MAX_DIM 64
 #define ORC_MAX_PARAMS 1024
 
-/* ---- float instantiation ---- */
+/* ---- float instantiation (libm single-precision functions) ---- */
 #define REAL float
 #define SFX _f32
 #define EXP expf
 #define FABS fabsf
+#define SIN sinf
+#define COS cosf
+#define TAN tanf
+#define TANH tanhf
+#define POW powf
+#define SQRT sqrtf
+#define LOG logf
+#define FMIN fminf
+#define FMAX fmaxf
 #include "oracle_impl.h"
 #undef REAL
 #undef SFX
 #undef EXP
 #undef FABS
+#undef SIN
+#undef COS
+#undef TAN
+#undef TANH
+#undef POW
+#undef SQRT
+#undef LOG
+#undef FMIN
+#undef FMAX
 
 /* ---- double instantiation ---- */
 #define REAL double
 #define SFX _f64
 #define EXP exp
 #define FABS fabs
+#define SIN sin
+#define COS cos
+#define TAN tan
+#define TANH tanh
+#define POW pow
+#define SQRT sqrt
+#define LOG log
+#define FMIN fmin
+#define FMAX fmax
 #include "oracle_impl.h"
 #undef REAL
 #undef SFX
 #undef EXP
 #undef FABS
+#undef SIN
+#undef COS
+#undef TAN
+#undef TANH
+#undef POW
+#undef SQRT
+#undef LOG
+#undef FMIN
+#undef FMAX
 
 /* =====================================================================================
  * Philox4x32-10 (Salmon et al., SC'11, "Parallel random numbers: as easy as 1, 2, 3";

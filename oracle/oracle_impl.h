@@ -114,6 +114,19 @@ static void F(rhs_hh)(int dim, const REAL* x, const REAL* p, REAL* dx) {
   }
 }
 
+/* Front-end coverage system (not from the paper; exercises every builtin function of the
+ * expression grammar in include/fireflies.h). p = {a, b}. Pinned only by closed-form values at the
+ * origin (tests/test_oracle_models.py) and the RK4 pins; otherwise "parity unpinned". */
+static void F(rhs_funcs)(int dim, const REAL* v, const REAL* p, REAL* dx) {
+  (void)dim;
+  const REAL x = v[0], y = v[1], z = v[2], a = p[0], b = p[1];
+  const REAL pi = (REAL)3.14159265358979323846, e = (REAL)2.71828182845904523536;
+  dx[0] = SIN(a * x) * COS(y) + TANH(z) - POW((REAL)1 + x * x, (REAL)0.75) + pi * (REAL)0.1;
+  dx[1] = SQRT((REAL)1 + y * y) - LOG((REAL)2 + SIN(x)) + EXP(-(b * (x * x))) + FABS(z - x) - (y * y * y) / (REAL)10;
+  dx[2] = FMIN(x, y) - FMAX(y, z) * ((REAL)1 / ((REAL)1 + EXP(-(x - z)))) + (x + y) / ((REAL)1 + z * z) +
+          TAN((REAL)0.3 * z) - e * (REAL)0.05 * z;
+}
+
 static int F(rhs_dispatch)(int model, int dim, const REAL* x, const REAL* p, REAL* dx) {
   switch (model) {
     case ORC_LINEAR: F(rhs_linear)(dim, x, p, dx); return 0;
@@ -121,6 +134,7 @@ static int F(rhs_dispatch)(int model, int dim, const REAL* x, const REAL* p, REA
     case ORC_LORENZ: if (dim != 3) return -1; F(rhs_lorenz)(dim, x, p, dx); return 0;
     case ORC_STN: if (dim != 2) return -1; F(rhs_stn)(dim, x, p, dx); return 0;
     case ORC_HH: if (dim < 5 || dim % 5 != 0) return -1; F(rhs_hh)(dim, x, p, dx); return 0;
+    case ORC_FUNCS: if (dim != 3) return -1; F(rhs_funcs)(dim, x, p, dx); return 0;
     default: return -1;
   }
 }

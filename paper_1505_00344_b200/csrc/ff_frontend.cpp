@@ -810,6 +810,8 @@ std::string emit_source(const System& s, int sweep_param) {
   int unroll = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
   int minb_p1 = dim <= 4 ? 4 : (dim <= 8 ? 3 : (dim <= 16 ? 2 : 1));
   int minb_p2 = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
+  int minb_p4 = dim <= 4 ? 6 : (dim <= 8 ? 2 : 1);   // 128-thread blocks (Lorenz: 76 regs, 6 blocks/SM)
+  if (const char* e = std::getenv("FF_TUNE_MINB_P4")) minb_p4 = std::atoi(e);
   // tuning knobs for experiments (not part of the ABI): FF_TUNE_MINB_P2, FF_TUNE_UNROLL
   if (const char* e = std::getenv("FF_TUNE_MINB_P2")) minb_p2 = std::atoi(e);
   if (const char* e = std::getenv("FF_TUNE_UNROLL")) unroll = std::atoi(e);
@@ -821,6 +823,7 @@ std::string emit_source(const System& s, int sweep_param) {
   pre << "#define FF_UNROLL " << unroll << "\n";
   pre << "#define FF_MINB_P1 " << minb_p1 << "\n";
   pre << "#define FF_MINB_P2 " << minb_p2 << "\n";
+  pre << "#define FF_MINB_P4 " << minb_p4 << "\n";
   pre << "#define FF_SWEEP " << sweep_param << "\n";
 
   std::string tmpl(kDeviceTemplate);
@@ -830,7 +833,8 @@ std::string emit_source(const System& s, int sweep_param) {
   std::string bcast =
       "template <class V> __device__ __forceinline__ V ff_bcast(float s);\n"
       "template <> __device__ __forceinline__ float ff_bcast<float>(float s) { return s; }\n"
-      "template <> __device__ __forceinline__ ff2 ff_bcast<ff2>(float s) { return ff2b(s); }\n";
+      "template <> __device__ __forceinline__ ff2 ff_bcast<ff2>(float s) { return ff2b(s); }\n"
+      "template <> __device__ __forceinline__ ff4 ff_bcast<ff4>(float s) { return ff4b(s); }\n";
   tmpl.replace(at, marker.size(), bcast + rhs.str());
   return pre.str() + tmpl;
 }

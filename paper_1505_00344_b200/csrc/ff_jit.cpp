@@ -102,7 +102,10 @@ std::vector<char> compile_cubin(const std::string& source, const std::string& na
   };
   nvrtcProgram prog;
   check(api.create(&prog, source.c_str(), name.c_str(), 0, nullptr, nullptr), "nvrtcCreateProgram");
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--use_fast_math", "--std=c++17", "-lineinfo",
+  // fast-math semantics for the arithmetic (FTZ, contraction, approximate division/sqrt), but NOT
+  // --use_fast_math's swap of sinf/cosf/logf/powf/tanhf for their coarse MUFU approximations
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-ftz=true", "-prec-div=false", "-prec-sqrt=false",
+                        "-fmad=true", "--std=c++17", "-lineinfo",
                         "--device-as-default-execution-space"};
   nvrtcResult rc = api.compile(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
   if (rc != NVRTC_SUCCESS) {

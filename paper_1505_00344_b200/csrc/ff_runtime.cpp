@@ -37,20 +37,22 @@ struct Module {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t init = nullptr;
   cudaKernel_t render = nullptr;
-  // step kernels by (ppt, tpb): index 0 p1t128, 1 p1t256, 2 p1t512, 3 p2t128, 4 p2t256
-  cudaKernel_t step[5] = {};
-  int occ[5] = {};
+  // step kernels by (ppt, tpb): 0 p1t128, 1 p1t256, 2 p1t512, 3 p2t128, 4 p2t256, 5 p4t128
+  cudaKernel_t step[6] = {};
+  int occ[6] = {};
 };
 
+constexpr int kNumStep = 6;
 int step_index(int ppt, int tpb) {
   if (ppt == 1) return tpb == 128 ? 0 : tpb == 256 ? 1 : tpb == 512 ? 2 : -1;
   if (ppt == 2) return tpb == 128 ? 3 : tpb == 256 ? 4 : -1;
+  if (ppt == 4) return tpb == 128 ? 5 : -1;
   return -1;
 }
-const char* kStepNames[5] = {"ff_step_p1_t128", "ff_step_p1_t256", "ff_step_p1_t512", "ff_step_p2_t128",
-                             "ff_step_p2_t256"};
-const int kStepPPT[5] = {1, 1, 1, 2, 2};
-const int kStepTPB[5] = {128, 256, 512, 128, 256};
+const char* kStepNames[kNumStep] = {"ff_step_p1_t128", "ff_step_p1_t256", "ff_step_p1_t512", "ff_step_p2_t128",
+                                    "ff_step_p2_t256", "ff_step_p4_t128"};
+const int kStepPPT[kNumStep] = {1, 1, 1, 2, 2, 4};
+const int kStepTPB[kNumStep] = {128, 256, 512, 128, 256, 128};
 
 struct GroupRec {
   int64_t n_global = 0, first_global = 0, n_local = 0, slot_begin = 0, slot_end = 0;
@@ -143,7 +145,7 @@ struct ff_ctx {
     ck(cudaLibraryLoadData(&m.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
     ck(cudaLibraryGetKernel(&m.init, m.lib, "ff_init"), "cudaLibraryGetKernel(ff_init)");
     ck(cudaLibraryGetKernel(&m.render, m.lib, "ff_render"), "cudaLibraryGetKernel(ff_render)");
-    for (int i = 0; i < 5; ++i) {
+    for (int i = 0; i < kNumStep; ++i) {
       ck(cudaLibraryGetKernel(&m.step[i], m.lib, kStepNames[i]), "cudaLibraryGetKernel(ff_step)");
       int occ = 0;
       cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m.step[i], kStepTPB[i], 0);
@@ -168,8 +170,8 @@ struct ff_ctx {
   void default_launch(int& ppt_out, int& tpb_out) const {
     // measured on B200: packed pairs win for the paper's systems; 15-D HH needs the
     // smaller block for its ~248-register pair kernel
-    ppt_out = ppt ? ppt : (sys.dim <= 16 ? 2 : 1);
-    tpb_out = tpb ? tpb : (sys.dim <= 8 ? 256 : 128);
+    ppt_out = ppt ? ppt : (sys.dim <= 4 ? 4 : (sys.dim <= 16 ? 2 : 1));
+    tpb_out = tpb ? tpb : (sys.dim <= 4 ? 128 : (sys.dim <= 8 ? 256 : 128));
   }
 
   void launch_step(int64_t n_steps, float dt) {
@@ -595,7 +597,7 @@ ff_status ff_step(ff_ctx* ctx, int64_t n_steps, float dt) {
 ff_status ff_set_launch(ff_ctx* ctx, int ppt, int tpb) {
   FF_TRY
   need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
-  need(ppt == 0 || ppt == 1 || ppt == 2, FF_ERR_INVALID_ARG, "particles per thread must be 0, 1 or 2");
+  need(ppt == 0 || ppt == 1 || ppt == 2 || ppt == 4, FF_ERR_INVALID_ARG, "particles per thread must be 0, 1, 2 or 4");
   need(tpb == 0 || tpb == 128 || tpb == 256 || tpb == 512, FF_ERR_INVALID_ARG, "threads per block must be 0/128/256/512");
   const int old_p = ctx->ppt, old_t = ctx->tpb;
   ctx->ppt = ppt;

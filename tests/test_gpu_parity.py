@@ -22,7 +22,7 @@ from paper_1505_00344_b200._abi import FFError, FF_ERR_RANGE, FF_ERR_STATE, FF_E
 
 LZ_LO, LZ_HI = [-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]   # Fig. 3A box
 LZ_P = np.array([10.0, 28.0, 8.0 / 3.0], np.float32)
-LAUNCHES = [(1, 128), (1, 256), (1, 512), (2, 128), (2, 256)]
+LAUNCHES = [(1, 128), (1, 256), (1, 512), (2, 128), (2, 256), (4, 128)]
 
 
 def lorenz_ctx(sizes, r=28.0):

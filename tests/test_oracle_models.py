@@ -259,3 +259,12 @@ def test_stn_backward_particles_leave():
     x = O.rk4(O.STN, rng.uniform(0, 1, (2, 500)), stn_p(), -0.01, 1000)
     out = np.any((x < 0) | (x > 1), axis=0)
     assert out.mean() > 0.95
+
+
+# ----------------------------------------------------------------------------- front-end coverage model
+def test_funcs_model_closed_form_at_origin():
+    # sin(0)cos(0) + tanh(0) - (1+0)^0.75 + 0.1 pi ; sqrt(1) - log(2) + exp(0) + |0| - 0 ; 0
+    d = O.rhs(O.FUNCS, [0.0, 0.0, 0.0], [1.3, 0.7])
+    np.testing.assert_allclose(d, [-1 + 0.1 * np.pi, 2 - np.log(2.0), 0.0], atol=1e-15)
+    d32 = O.rhs(O.FUNCS, [0.0, 0.0, 0.0], [1.3, 0.7], dtype=np.float32)
+    np.testing.assert_allclose(d32, d, atol=1e-6)
