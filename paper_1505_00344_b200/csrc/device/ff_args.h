@@ -52,6 +52,10 @@ struct FFStepArgs {
   ff_u32* epoch;        // per slot: resets so far (library-owned)
   float* birth;         // per slot: group time of the last (re)initialisation (library-owned)
   const float* ic_box;  // [group][lo | hi | top][dim] (library-owned)
+  // dynamic tile scheduler: a monotonically increasing 64-bit counter (library-owned); this launch
+  // owns the fetch numbers [tile_base, tile_base + tiles + grid)
+  ff_u64* tile_ctr;
+  ff_u64 tile_base;
   float bound_lo[FF_MAX_DIM_], bound_hi[FF_MAX_DIM_];
   FFGroup g[FF_MAX_GROUPS_];
   float p[FF_NP_ALLOC]; // parameter values (must stay the last member)

@@ -18,7 +18,7 @@
 #include "ff_internal.hpp"
 
 static_assert(sizeof(FFGroup) == 104, "FFGroup layout");
-static_assert(offsetof(FFStepArgs, g) == 688, "FFStepArgs layout");
+static_assert(offsetof(FFStepArgs, g) == 704, "FFStepArgs layout");
 static_assert(FF_MAX_DIM_ == FF_MAX_DIM, "bounds table size");
 static_assert(FF_MAX_GROUPS_ == FF_MAX_GROUPS, "group table size");
 
@@ -97,11 +97,15 @@ struct ff_ctx {
   float* birth = nullptr;
   float* ic_box = nullptr;
   std::vector<double> t_elapsed;  // per group: simulated time since creation (sum of |dt| n)
+  // dynamic tile scheduler counter (library-owned, 8 bytes) and the fetch numbers used so far
+  unsigned long long* tile_ctr = nullptr;
+  uint64_t tile_base = 0;
 
   ~ff_ctx() {
     for (auto& m : modules)
       if (m.second.lib) cudaLibraryUnload(m.second.lib);
     free_reset_buffers();
+    if (tile_ctr) cudaFree(tile_ctr);
   }
 
   void free_reset_buffers() {
@@ -202,6 +206,8 @@ struct ff_ctx {
     a.epoch = epoch;
     a.birth = birth;
     a.ic_box = ic_box;
+    a.tile_ctr = tile_ctr;
+    a.tile_base = tile_base;
     for (size_t d = 0; d < bound_lo.size(); ++d) {
       a.bound_lo[d] = bound_lo[d];
       a.bound_hi[d] = bound_hi[d];
@@ -238,6 +244,7 @@ struct ff_ctx {
     const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
     void* args[] = {&a};
     ck(cudaLaunchKernel((const void*)m.step[si], dim3(grid), dim3(t), args, 0, stream), "launch ff_step");
+    tile_base += (uint64_t)ntiles + grid;  // every block fetches until it sees a tile >= ntiles
     ++launches;
   }
 };
@@ -326,6 +333,8 @@ ff_status ff_create(const ff_system* sys, int device, ff_ctx** out) {
     c->device = device;
     ck(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
     c->module(-1);
+    ck(cudaMalloc(&c->tile_ctr, sizeof(unsigned long long)), "cudaMalloc tile counter");
+    ck(cudaMemset(c->tile_ctr, 0, sizeof(unsigned long long)), "cudaMemset tile counter");
   } catch (...) {
     delete c;
     throw;
