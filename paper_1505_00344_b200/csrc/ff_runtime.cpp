@@ -171,10 +171,16 @@ struct ff_ctx {
     return groups[gid];
   }
 
-  void default_launch(int& ppt_out, int& tpb_out) const {
+  void default_launch(int& ppt_out, int& tpb_out, int64_t n_steps = 100) const {
+    // memory-bound launches (1-4 steps) of small systems: 16-byte vector I/O, 4 particles/thread
+    if (!ppt && !tpb && sys.dim <= 4 && n_steps <= 4) {
+      ppt_out = 4;
+      tpb_out = 128;
+      return;
+    }
     // measured on B200: packed pairs win for the paper's systems; 15-D HH needs the
     // smaller block for its ~248-register pair kernel
-    ppt_out = ppt ? ppt : (sys.dim <= 4 ? 4 : (sys.dim <= 16 ? 2 : 1));
+    ppt_out = ppt ? ppt : (sys.dim <= 16 ? 2 : 1);
     tpb_out = tpb ? tpb : (sys.dim <= 4 ? 128 : (sys.dim <= 8 ? 256 : 128));
   }
 
@@ -182,7 +188,7 @@ struct ff_ctx {
     if (groups.empty()) throw ff::Error(FF_ERR_STATE, "no particle groups");
     if (!std::isfinite(dt)) throw ff::Error(FF_ERR_INVALID_ARG, "dt is not finite");
     int p, t;
-    default_launch(p, t);
+    default_launch(p, t, n_steps);
     const int si = step_index(p, t);
     Module& m = module(sweep_param);
     FFStepArgs a;
