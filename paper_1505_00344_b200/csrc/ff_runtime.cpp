@@ -212,7 +212,8 @@ struct ff_ctx {
     a.epoch = epoch;
     a.birth = birth;
     a.ic_box = ic_box;
-    a.tile_ctr = tile_ctr;
+    const bool dynamic_tiles = n_steps >= 8;  // long tiles: balance SMs with the global counter
+    a.tile_ctr = dynamic_tiles ? tile_ctr : nullptr;
     a.tile_base = tile_base;
     for (size_t d = 0; d < bound_lo.size(); ++d) {
       a.bound_lo[d] = bound_lo[d];
@@ -250,7 +251,7 @@ struct ff_ctx {
     const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
     void* args[] = {&a};
     ck(cudaLaunchKernel((const void*)m.step[si], dim3(grid), dim3(t), args, 0, stream), "launch ff_step");
-    tile_base += (uint64_t)ntiles + grid;  // every block fetches until it sees a tile >= ntiles
+    if (dynamic_tiles) tile_base += (uint64_t)ntiles + grid;  // each block fetches until a tile >= ntiles
     ++launches;
   }
 };
