@@ -212,8 +212,7 @@ struct ff_ctx {
     a.epoch = epoch;
     a.birth = birth;
     a.ic_box = ic_box;
-    const bool dynamic_tiles = n_steps >= 8;  // long tiles: balance SMs with the global counter
-    a.tile_ctr = dynamic_tiles ? tile_ctr : nullptr;
+    a.tile_ctr = tile_ctr;
     a.tile_base = tile_base;
     for (size_t d = 0; d < bound_lo.size(); ++d) {
       a.bound_lo[d] = bound_lo[d];
@@ -251,7 +250,7 @@ struct ff_ctx {
     const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
     void* args[] = {&a};
     ck(cudaLaunchKernel((const void*)m.step[si], dim3(grid), dim3(t), args, 0, stream), "launch ff_step");
-    if (dynamic_tiles) tile_base += (uint64_t)ntiles + grid;  // each block fetches until a tile >= ntiles
+    tile_base += (uint64_t)ntiles + grid;  // each block fetches until it sees a tile >= ntiles
     ++launches;
   }
 };
