@@ -810,10 +810,10 @@ std::string emit_source(const System& s, int sweep_param) {
   int unroll = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
   int minb_p1 = dim <= 4 ? 4 : (dim <= 8 ? 3 : (dim <= 16 ? 2 : 1));
   int minb_p2 = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
-  // 128-thread packed kernel: for small systems force high occupancy (12 blocks = 48 warps/SM,
-  // <= 40 registers; 16 blocks / 32 registers is as fast but one edit away from spilling in the
-  // loop): measured best for Lorenz on B200 (~89.6% of the FMA pipe vs 87.2% at 46 registers)
-  int minb_p2_t128 = dim <= 4 ? 12 : (dim <= 8 ? 4 : 2);
+  // 128-thread packed kernel: for small systems force full occupancy (16 blocks = 64 warps/SM,
+  // <= 32 registers): measured best for Lorenz on B200 (89.6% of the FMA pipe; 12 blocks / 37
+  // registers: 87.9%). tests/test_sass.py checks that the inner loop does not spill.
+  int minb_p2_t128 = dim <= 4 ? 16 : (dim <= 8 ? 4 : 2);
   if (const char* e = std::getenv("FF_TUNE_MINB_P2_T128")) minb_p2_t128 = std::atoi(e);
   int minb_p4 = dim <= 4 ? 6 : (dim <= 8 ? 2 : 1);   // 128-thread blocks (Lorenz: 76 regs, 6 blocks/SM)
   if (const char* e = std::getenv("FF_TUNE_MINB_P4")) minb_p4 = std::atoi(e);

@@ -1,0 +1,51 @@
+"""SASS checks of the generated kernels (CPU only: NVRTC + cuobjdump): the inner RK4 loop of the
+default Lorenz kernel issues exactly the expected FMA-pipe work, packed, without spills."""
+import collections
+import re
+import subprocess
+
+import pytest
+
+import paper_1505_00344_b200 as FF
+from paper_1505_00344_b200 import systems
+
+
+def inner_loops(cubin_path, kernel):
+    sass = subprocess.run(["cuobjdump", "-sass", "-fun", kernel, cubin_path], capture_output=True, text=True).stdout
+    ins = []
+    for ln in sass.splitlines():
+        m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(@!?U?P\w+\s+)?([A-Z0-9_.]+)(.*?);", ln)
+        if m:
+            ins.append((int(m.group(1), 16), m.group(3), m.group(4)))
+    loops = []
+    for a, op, rest in ins:
+        if op.startswith("BRA"):
+            t = re.search(r"0x([0-9a-f]+)", rest)
+            if t and int(t.group(1), 16) < a:
+                lo = int(t.group(1), 16)
+                loops.append(collections.Counter(o.split(".")[0] for (b, o, _) in ins if lo <= b <= a))
+    return loops
+
+
+@pytest.fixture(scope="module")
+def lorenz_cubin(tmp_path_factory):
+    p = tmp_path_factory.mktemp("sass") / "lorenz.cubin"
+    p.write_bytes(FF.ff_compile_cubin(systems.lorenz()))
+    return str(p)
+
+
+def test_packed_loop_is_44_lane_ops_per_particle_step_no_spills(lorenz_cubin):
+    loops = [c for c in inner_loops(lorenz_cubin, "ff_step_p2_t128") if c["FFMA2"] >= 100]
+    assert loops, "no packed RK4 loop found"
+    main = min(loops, key=lambda c: sum(c.values()))   # innermost = the smallest loop body
+    packed = main["FFMA2"] + main["FMUL2"] + main["FADD2"]
+    # unrolled x4, two particles per instruction: 4 steps x 2 particles x 44 lane-ops / 2 lanes
+    assert packed == 176
+    assert main["LDL"] == 0 and main["STL"] == 0
+    assert main["FFMA"] == 0 and main["FADD"] == 0 and main["FMUL"] == 0   # nothing left unpacked
+
+
+def test_scalar_loop_is_44_ops(lorenz_cubin):
+    loops = [c for c in inner_loops(lorenz_cubin, "ff_step_p1_t256") if c["FFMA"] >= 100]
+    main = min(loops, key=lambda c: sum(c.values()))
+    assert main["FFMA"] + main["FADD"] + main["FMUL"] == 176 and main["LDL"] == 0
