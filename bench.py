@@ -37,33 +37,33 @@ XU_LANES = 16     # MUFU results per clock per SM (same microbenchmark)
 WORKLOADS = {
     "lorenz3d": dict(system="lorenz", groups=[(1 << 22, 1, 0, 2), (1 << 22, -1, 1, 3)], params={"r": 28.0},
                      box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj="lorenz_camera", W=1024, H=1024, C=2,
-                     S=100, dt=0.01, fma_ops=45, mufu_ops=0, bound="alu",
+                     S=100, dt=0.01,
                      desc="Lorenz r=28, 4M fwd + 4M bwd, 3-D perspective image 1024x1024x2"),
     "stn": dict(system="stn_gpe", groups=[(5000, 1, 0, 1), (5000, -1, 1, 11)], params={},
                 box=([0.0, 0.0], [1.0, 1.0]), proj=([0, 1], [0.0, 1.0, 0.0, 1.0]), W=512, H=512, C=2,
-                S=1000, dt=0.01, fma_ops=None, mufu_ops=16, bound="xu",
+                S=1000, dt=0.01, 
                 desc="STN-GPe 5k fwd + 5k bwd, 1000 steps, 2-D image 512x512x2 (configs[0])"),
     "hh": dict(system="hh_ring3", groups=[(1 << 20, 1, 0, 4)], params={},
                box=([-20.0, 0, 0, 0, 0] * 3, [100.0, 1, 1, 1, 1] * 3), proj=([0, 5], [-20.0, 120.0, -20.0, 120.0]),
-               W=1024, H=1024, C=1, S=100, dt=0.01, fma_ops=None, mufu_ops=132, bound="xu",
+               W=1024, H=1024, C=1, S=100, dt=0.01,
                desc="HH ring N=3 (15-D), 1M particles, 2-D (V1,V2) image 1024x1024 (configs[2])"),
     "sweep": dict(system="lorenz", groups=[(1 << 24, 1, 0, 5)], params={}, sweep=("r", 0.0, 200.0, 0, 5),
                   box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj=([3, 1], [0.0, 200.0, -160.0, 160.0]),
-                  W=2048, H=1024, C=1, S=100, dt=0.01, fma_ops=45, mufu_ops=0, bound="alu",
+                  W=2048, H=1024, C=1, S=100, dt=0.01,
                   desc="Lorenz r swept in [0,200), 16M particles, (r, y) image 2048x1024 (configs[3])"),
     "lorenz3d_collapsed": dict(system="lorenz", groups=[(1 << 22, 1, 0, 2), (1 << 22, 1, 1, 3)], params={"r": 0.5},
                                box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj="lorenz_camera", W=1024, H=1024,
-                               C=2, S=100, dt=0.01, fma_ops=45, mufu_ops=0, bound="alu", prerun=4000,
+                               C=2, S=100, dt=0.01, prerun=4000,
                                desc="Lorenz r=0.5 after 4000 steps: 8M particles in ~1 pixel (histogram stress)"),
     "stn_bif3d": dict(system="stn_gpe", groups=[(1 << 22, 1, 0, 21), (1 << 22, -1, 1, 22)], params={},
                       sweep=("w_ss", 0.0, 12.0, 0, 23), reset=([0.0, 0.0], [1.0, 1.0], 0.0),
                       box=([0.0, 0.0], [1.0, 1.0]), proj="stn_box_camera", W=1024, H=1024, C=2, S=100, dt=0.01,
-                      fma_ops=None, mufu_ops=16, bound="xu",
+                      
                       desc="STN-GPe 3-D bifurcation (x, y, w_ss in [0,12)), 4M fwd + 4M bwd with reset "
                            "(PAPER.md:54, :59; NEXT row 4)"),
     "lorenz1b": dict(system="lorenz", groups=[(1 << 30, 1, 0, 6)], params={"r": 28.0}, strong=True,
                      box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj="lorenz_camera", W=1024, H=1024, C=1,
-                     S=100, dt=0.01, fma_ops=45, mufu_ops=0, bound="alu",
+                     S=100, dt=0.01,
                      desc="Lorenz 1B particles sharded over the GPUs (configs[4])"),
 }
 
@@ -216,7 +216,7 @@ def run_ours(args, w, rank, world, device):
 
     # end-to-end through the C ABI with host buffers: pinned host state in, image out, every frame
     e2e = None
-    if not dist and not args.no_e2e:
+    if not args.no_e2e:
         host_in = [torch.from_numpy(ctx.read_state(g)).pin_memory() for g in gids]
         host_img = torch.empty(tuple(img.shape), dtype=torch.int32).pin_memory()
         h2d = sum(t.numel() * 4 for t in host_in)
@@ -228,11 +228,15 @@ def run_ours(args, w, rank, world, device):
                 F.check(F.lib().ff_write_state(ctx.ctx, g, 0, t.shape[1], F.C.c_void_p(t.data_ptr())))
             img.zero_()
             ctx.step(S, w["dt"])
+            if dist:
+                torch.distributed.all_reduce(img)
             F.ff_read_image_into(ctx.ctx, host_img.data_ptr())
 
         for _ in range(2):
             e2e_frame()
         ke = max(3, min(args.steps, 20))
+        if dist:
+            torch.distributed.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -241,8 +245,14 @@ def run_ours(args, w, rank, world, device):
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / ke
-        e2e = {"value": n_local * S / (ms * 1e-3), "unit": "particle-steps/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": ms}
+        if dist:
+            t = torch.tensor([ms], dtype=torch.float64, device=device)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        e2e = {"value": n_total * S / (ms * 1e-3), "unit": "particle-steps/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+               "path": "per frame: ff_write_state (pinned host -> device, whole state), ff_step, "
+                       + ("NCCL image all-reduce, " if dist else "") + "ff_read_image (device -> pinned host)"}
     im_sum = int(img.sum().item())
     ctx.close()
     sweep_idx = -1

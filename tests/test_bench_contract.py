@@ -1,0 +1,38 @@
+"""bench.py contract checks that run without a GPU: the reference arm (the oracle on the host cores)
+prints one JSON line with the driver's keys; the workloads match BASELINE.json's configs."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "1", "--config", "stn"], capture_output=True, text=True, timeout=600,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["config"]["workload"] == "stn"
+
+
+def test_workloads_cover_baseline_configs():
+    sys.path.insert(0, ROOT)
+    import bench
+    base = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+    assert len(base["configs"]) == 5
+    w = bench.WORKLOADS
+    assert sum(n for n, *_ in w["stn"]["groups"]) == 10000                          # configs[0]
+    assert [g[0] for g in w["lorenz3d"]["groups"]] == [1 << 22, 1 << 22]            # configs[1]
+    assert w["lorenz3d"]["groups"][1][1] == -1 and w["lorenz3d"]["proj"] == "lorenz_camera"
+    assert w["hh"]["groups"][0][0] == 1 << 20 and len(w["hh"]["box"][0]) == 15      # configs[2]
+    assert w["sweep"]["groups"][0][0] == 1 << 24 and w["sweep"]["sweep"][1:3] == ("r", 0.0, 200.0)[1:]  # configs[3]
+    assert w["lorenz1b"]["groups"][0][0] == 1 << 30 and w["lorenz1b"].get("strong")  # configs[4]
