@@ -235,6 +235,17 @@ ff_status ff_read_image(ff_ctx* ctx, uint32_t* host_image);
  * float[3][H][W] (caller-owned). Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE (no image), FF_ERR_CUDA. */
 ff_status ff_render(ff_ctx* ctx, const float* colours, float intensity, float radius_px, float* dev_rgb);
 
+/* Position-linear colour (the colour "varies linearly as a function of the
+ * particle's position in state space"). Once bound (after ff_project), every ff_step
+ * also adds, for each counted particle, q_k = min(255, floor(256 * clamp((v_k - lo_k) * s_k, 0, 1)))
+ * to colour_img[k][iy][ix], k = 0, 1, 2 over the projected axes (2-D: q_2 = 128), with
+ * s_k = 1 / (hi_k - lo_k) computed in float; all ops exact IEEE, counts integer (bit-exact). While a
+ * colour image is bound, ff_render uses it: rgb_k = min(1, intensity * sum_q colsum_k w(q) / 255).
+ * lo, hi: HOST arrays of n_axes floats (lo < hi). dev_colour_img: DEVICE uint32 [3][H][W],
+ * caller-owned, caller zeroes it; NULL unbinds. Sums overflow past 16.8 M particles in one pixel.
+ * Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE (no image bound). */
+ff_status ff_project_colour(ff_ctx* ctx, const float* lo, const float* hi, uint32_t* dev_colour_img);
+
 /* Number of kernel launches this context has issued (for bench evidence). */
 ff_status ff_launch_count(ff_ctx* ctx, int64_t* count);
 

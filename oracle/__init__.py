@@ -200,3 +200,38 @@ def render(image, colours, intensity, radius):
     if L.orc_render_f32(_ptr(img), W, H, C_, _ptr(col), intensity, radius, _ptr(out)) != 0:
         raise ValueError("orc_render_f32 rejected its arguments")
     return out
+
+
+def colour_histogram(x_soa, axes, view, W, H, lo, hi, colour=None, sweep_vals=None):
+    """Add position-colour sums into colour (3, H, W) uint32 (fireflies_oracle.c)."""
+    L = lib()
+    L.orc_colour_histogram_f32.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,
+                                           C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                           C.c_void_p]
+    L.orc_colour_histogram_f32.restype = C.c_int
+    x = np.ascontiguousarray(x_soa, dtype=np.float32)
+    dim, n = x.shape
+    if colour is None:
+        colour = np.zeros((3, H, W), np.uint32)
+    ax = np.ascontiguousarray(axes, dtype=np.int32)
+    vw = np.ascontiguousarray(view, dtype=np.float32)
+    lo_a = np.ascontiguousarray(lo, dtype=np.float32)
+    hi_a = np.ascontiguousarray(hi, dtype=np.float32)
+    sv = None if sweep_vals is None else np.ascontiguousarray(sweep_vals, dtype=np.float32)
+    rc = L.orc_colour_histogram_f32(_ptr(x), n, n, dim, _ptr(sv), _ptr(ax), ax.size, _ptr(vw), W, H, _ptr(lo_a),
+                                    _ptr(hi_a), _ptr(colour))
+    if rc != 0:
+        raise ValueError("orc_colour_histogram_f32 rejected its arguments")
+    return colour
+
+
+def render_colour(colour, intensity, radius):
+    L = lib()
+    L.orc_render_colour_f32.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_float, C.c_void_p]
+    L.orc_render_colour_f32.restype = C.c_int
+    col = np.ascontiguousarray(colour, dtype=np.uint32)
+    _, H, W = col.shape
+    out = np.empty((3, H, W), np.float32)
+    if L.orc_render_colour_f32(_ptr(col), W, H, intensity, radius, _ptr(out)) != 0:
+        raise ValueError("orc_render_colour_f32 rejected its arguments")
+    return out

@@ -370,4 +370,67 @@ int orc_render_f32(const uint32_t* image, int W, int H, int C, const float* colo
   return 0;
 }
 
+/* Position-linear colour ("varies linearly as a function of the particle's
+ * position"; reading R26): for every particle kept by the binning rule, add
+ *   q_k = min(255, floor(256 * clamp((v_k - lo_k) * s_k, 0, 1))),  s_k = 1 / (hi_k - lo_k) (float)
+ * to colour[k][bin] for the n_axes projected axes (2-D: q_2 = 128). */
+int orc_colour_histogram_f32(const float* x_soa, int64_t n, int64_t pitch, int dim, const float* sweep_vals,
+                             const int* axes, int n_axes, const float* view, int W, int H, const float* lo,
+                             const float* hi, uint32_t* colour) {
+  if (n_axes != 2 && n_axes != 3) return -1;
+  float s[3] = {0, 0, 0};
+  for (int k = 0; k < n_axes; ++k) {
+    if (!(lo[k] < hi[k])) return -1;
+    s[k] = 1.0f / (hi[k] - lo[k]);
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    float v[3];
+    for (int k = 0; k < n_axes; ++k) {
+      if (axes[k] < 0 || axes[k] > dim || (axes[k] == dim && !sweep_vals)) return -1;
+      v[k] = (axes[k] == dim) ? sweep_vals[i] : x_soa[(int64_t)axes[k] * pitch + i];
+    }
+    const int64_t b = (n_axes == 2) ? bin_2d(v, view, W, H) : bin_3d(v, view, W, H);
+    if (b < 0) continue;
+    for (int k = 0; k < 3; ++k) {
+      uint32_t q = 128u;
+      if (k < n_axes) {
+        float t = (v[k] - lo[k]) * s[k];
+        if (!(t > 0.0f)) t = 0.0f;
+        if (!(t < 1.0f)) t = 1.0f;
+        const float f = floorf(t * 256.0f);
+        q = f > 255.0f ? 255u : (uint32_t)f;
+      }
+      colour[(int64_t)k * H * W + b] += q;
+    }
+  }
+  return 0;
+}
+
+/* Render of position-colour sums: rgb_k = min(1, intensity * sum_taps colour_k w / 255) (taps, order
+ * and weights as orc_render_f32). */
+int orc_render_colour_f32(const uint32_t* colour, int W, int H, float intensity, float radius, float* rgb) {
+  if (W < 1 || H < 1 || !(radius > 0.0f) || radius > 8.0f) return -1;
+  const int hw = (int)ceil((double)radius);
+  for (int k = 0; k < 3; ++k) {
+    for (int y = 0; y < H; ++y) {
+      for (int x = 0; x < W; ++x) {
+        double acc = 0.0;
+        for (int dy = -hw; dy <= hw; ++dy) {
+          for (int dx = -hw; dx <= hw; ++dx) {
+            const int yy = y + dy, xx = x + dx;
+            if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+            const double r = sqrt((double)(dx * dx + dy * dy)) / (double)radius;
+            const double f = 1.0 - (r < 1.0 ? r : 1.0);
+            const float w = (float)(f * f);
+            acc = acc + (double)colour[((int64_t)k * H + yy) * W + xx] * (double)w;
+          }
+        }
+        const double v = ((double)intensity * acc) / 255.0;
+        rgb[((int64_t)k * H + y) * W + x] = (float)(v < 1.0 ? v : 1.0);
+      }
+    }
+  }
+  return 0;
+}
+
 int orc_version(void) { return 1; }

@@ -23,7 +23,7 @@ EXPORTS = ["ff_last_error", "ff_abi_version", "ff_build_info", "ff_emit_source",
            "ff_set_stream", "ff_set_shard", "ff_shard_range", "ff_bind_state", "ff_group_slots", "ff_init_group", "ff_group_info",
            "ff_set_param", "ff_get_param", "ff_sweep_param", "ff_project", "ff_step", "ff_set_reset",
            "ff_read_epochs", "ff_set_launch",
-           "ff_read_state", "ff_write_state", "ff_read_image", "ff_render", "ff_launch_count", "ff_sync"]
+           "ff_read_state", "ff_write_state", "ff_read_image", "ff_render", "ff_project_colour", "ff_launch_count", "ff_sync"]
 
 
 class FFError(RuntimeError):
@@ -79,6 +79,7 @@ def lib():
             "ff_write_state": ([P, i32, i64, i64, P], C.c_int),
             "ff_read_image": ([P, P], C.c_int),
             "ff_render": ([P, P, f32, f32, P], C.c_int),
+            "ff_project_colour": ([P, P, P, P], C.c_int),
             "ff_launch_count": ([P, C.POINTER(i64)], C.c_int),
             "ff_sync": ([P], C.c_int),
         }

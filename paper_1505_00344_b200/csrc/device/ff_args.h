@@ -56,6 +56,11 @@ struct FFStepArgs {
   // owns the fetch numbers [tile_base, tile_base + tiles + grid)
   ff_u64* tile_ctr;
   ff_u64 tile_base;
+  // position-linear colour: per particle q_k = min(255, floor(256 * clamp((v_k -
+  // lo_k) * s_k, 0, 1))) of its projected axis values, summed per pixel into colour_img[3][H][W]
+  ff_u32* colour_img;   // null = off
+  float col_lo[3], col_s[3];
+  int pad2_;
   float bound_lo[FF_MAX_DIM_], bound_hi[FF_MAX_DIM_];
   FFGroup g[FF_MAX_GROUPS_];
   float p[FF_NP_ALLOC]; // parameter values (must stay the last member)
@@ -66,6 +71,7 @@ struct FFStepArgs {
 #define FF_RENDER_MAX_C 16
 struct FFRenderArgs {
   const ff_u32* image;  // [C][H][W] counts
+  const ff_u32* colour_img;  // [3][H][W] position-colour sums (q in 0..255 per particle) or null
   float* rgb;           // [3][H][W] output
   int W, H, C, hw;      // hw = half width of the sprite footprint in pixels
   float intensity;      // sprite alpha

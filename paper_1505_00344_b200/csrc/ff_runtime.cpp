@@ -18,7 +18,7 @@
 #include "ff_internal.hpp"
 
 static_assert(sizeof(FFGroup) == 104, "FFGroup layout");
-static_assert(offsetof(FFStepArgs, g) == 704, "FFStepArgs layout");
+static_assert(offsetof(FFStepArgs, g) == 744, "FFStepArgs layout");
 static_assert(FF_MAX_DIM_ == FF_MAX_DIM, "bounds table size");
 static_assert(FF_MAX_GROUPS_ == FF_MAX_GROUPS, "group table size");
 
@@ -86,6 +86,8 @@ struct ff_ctx {
   float view[16] = {};
   int W = 0, H = 0, C = 0;
   uint32_t* image = nullptr;
+  uint32_t* colour_img = nullptr;  // position-linear colour sums [3][H][W] (ff_project_colour)
+  float col_lo[3] = {0, 0, 0}, col_s[3] = {0, 0, 0};
   float s0 = 0, s1 = 0;
   int ppt = 0, tpb = 0;
   int64_t launches = 0;
@@ -198,6 +200,11 @@ struct ff_ctx {
     a.slots_total = next_slot;
     a.n_steps = n_steps;
     a.image = image;
+    a.colour_img = image ? colour_img : nullptr;
+    for (int k = 0; k < 3; ++k) {
+      a.col_lo[k] = col_lo[k];
+      a.col_s[k] = col_s[k];
+    }
     a.proj = image ? proj : 0;
     a.W = W;
     a.H = H;
@@ -246,10 +253,20 @@ struct ff_ctx {
     const int64_t tile = (int64_t)p * t;
     const int64_t ntiles = next_slot / tile;
     if (ntiles == 0) return;
-    const int64_t resident = (int64_t)nsm * m.occ[si];
+    // position-linear colour: 3 extra per-block table planes in dynamic shared memory
+    const size_t dyn_smem = (image && colour_img) ? 3 * 1024 * sizeof(uint32_t) : 0;
+    int occ = m.occ[si];
+    if (dyn_smem) {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m.step[si], t, dyn_smem) != cudaSuccess) {
+        cudaGetLastError();
+        occ = 1;
+      }
+      occ = occ > 0 ? occ : 1;
+    }
+    const int64_t resident = (int64_t)nsm * occ;
     const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
     void* args[] = {&a};
-    ck(cudaLaunchKernel((const void*)m.step[si], dim3(grid), dim3(t), args, 0, stream), "launch ff_step");
+    ck(cudaLaunchKernel((const void*)m.step[si], dim3(grid), dim3(t), args, dyn_smem, stream), "launch ff_step");
     tile_base += (uint64_t)ntiles + grid;  // each block fetches until it sees a tile >= ntiles
     ++launches;
   }
@@ -565,6 +582,7 @@ ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view
   need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
   if (!image) {
     ctx->image = nullptr;
+    ctx->colour_img = nullptr;
     ctx->proj = 0;
     return FF_OK;
   }
@@ -598,6 +616,30 @@ ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view
   ctx->C = C;
   ctx->image = image;
   if (!ctx->groups.empty()) ctx->launch_step(0, 0.0f);
+  FF_CATCH
+}
+
+ff_status ff_project_colour(ff_ctx* ctx, const float* lo, const float* hi, uint32_t* dev_colour_img) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  if (!dev_colour_img) {
+    ctx->colour_img = nullptr;
+    return FF_OK;
+  }
+  need(ctx->image != nullptr, FF_ERR_STATE, "bind an image with ff_project first");
+  need(lo && hi, FF_ERR_INVALID_ARG, "lo / hi is NULL");
+  need(((uintptr_t)dev_colour_img & 3) == 0, FF_ERR_INVALID_ARG, "colour image must be 4-byte aligned");
+  for (int k = 0; k < 3; ++k) {
+    ctx->col_lo[k] = 0.0f;
+    ctx->col_s[k] = 0.0f;
+  }
+  for (int k = 0; k < ctx->proj; ++k) {
+    need(std::isfinite(lo[k]) && std::isfinite(hi[k]) && lo[k] < hi[k], FF_ERR_INVALID_ARG,
+         "colour range needs finite lo < hi per axis");
+    ctx->col_lo[k] = lo[k];
+    ctx->col_s[k] = 1.0f / (hi[k] - lo[k]);
+  }
+  ctx->colour_img = dev_colour_img;
   FF_CATCH
 }
 
@@ -668,6 +710,7 @@ ff_status ff_render(ff_ctx* ctx, const float* colours, float intensity, float ra
   FFRenderArgs a;
   std::memset(&a, 0, sizeof a);
   a.image = ctx->image;
+  a.colour_img = ctx->colour_img;
   a.rgb = dev_rgb;
   a.W = ctx->W;
   a.H = ctx->H;

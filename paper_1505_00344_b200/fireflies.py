@@ -274,6 +274,18 @@ class Context:
         ff_read_image_into(self.ctx, out.ctypes.data)
         return out
 
+    def project_colour(self, lo, hi, colour_image=None):
+        """Bind (zero-allocating if needed) the position-colour sums [3][H][W] (ff_project_colour)."""
+        torch = self.torch
+        C_, H, W = self.image.shape
+        if colour_image is None:
+            colour_image = torch.zeros((3, H, W), dtype=torch.int32, device=self.device)
+        lo_a = np.ascontiguousarray(lo, dtype=np.float32)
+        hi_a = np.ascontiguousarray(hi, dtype=np.float32)
+        check(lib().ff_project_colour(self.ctx, _fptr(lo_a), _fptr(hi_a), C.c_void_p(colour_image.data_ptr())))
+        self.colour_image = colour_image
+        return colour_image
+
     def render(self, colours, intensity=1.0, radius_px=2.0, out=None):
         """RGB float32 [3][H][W] frame of the bound image (device tensor)."""
         torch = self.torch

@@ -37,6 +37,32 @@ def test_render_bit_exact(radius):
     assert rgb.max() == 1.0 and rgb.min() == 0.0
 
 
+@pytest.mark.parametrize("ppt,tpb", [(2, 128), (4, 128), (1, 256)])
+def test_position_colour_bit_exact(ppt, tpb):
+    # colour linear in position: per-pixel colour sums and their render,
+    # written through identical host state, bit-exact vs the oracle; includes a hot pixel (table path)
+    n = 40000 + 1
+    rng = np.random.default_rng(81)
+    ctx = FF.Context(systems.lorenz(), [n])
+    ctx.set_launch(ppt, tpb)
+    g = ctx.init_group([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0], n, 1, 0, seed=2)
+    x = np.vstack([rng.normal(0, 8, n), rng.normal(0, 20, n), rng.uniform(0, 50, n)]).astype(np.float32)
+    x[:, :8000] = np.array([[1.0], [2.0], [25.0]], np.float32)     # 8000 particles in one pixel
+    ctx.write_state(g, x)
+    M = views.lorenz_camera()
+    img = ctx.project([0, 1, 2], M, 300, 300, 1)
+    lo, hi = [-20.0, -30.0, 0.0], [20.0, 30.0, 50.0]
+    col = ctx.project_colour(lo, hi)
+    img.zero_()
+    ctx.step(0, 0.01)   # bin-only launch (n = 0) with colour bound
+    ctx.sync()
+    want_c = O.colour_histogram(x, [0, 1, 2], M, 300, 300, lo, hi)
+    assert np.array_equal(col.cpu().numpy().view(np.uint32), want_c)
+    assert np.array_equal(ctx.read_image(), O.histogram(x, [0, 1, 2], M, 300, 300, 1, 0))
+    rgb = ctx.render([[1, 1, 1]], 0.01, 2.0).cpu().numpy()
+    assert np.array_equal(rgb.view(np.uint32), O.render_colour(want_c, 0.01, 2.0).view(np.uint32))
+
+
 def test_render_after_fused_step_properties():
     # after a real fused launch: frame in [0, 1], lit exactly where the sprite footprint of a counted
     # pixel reaches (properties only -- the oracle never takes the GPU image as input)

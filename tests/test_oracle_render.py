@@ -28,6 +28,17 @@ def test_additive_blending_and_saturation():
     assert rgb[0, 4, 4] == 1.0 and rgb[1, 4, 4] == 1.0 and rgb[2].max() == 0.0
 
 
+def test_position_colour_hand_values():
+    # colour linear in position: q = min(255, floor(256 clamp((v - lo)/(hi - lo), 0, 1)))
+    x = np.array([[0.0, 0.25, 0.999, 1.0, -0.5], [0.5, 0.5, 0.5, 0.5, 0.5]], np.float32)
+    c = O.colour_histogram(x, [0, 1], [-1.0, 2.0, 0.0, 1.0], 3, 1, [0.0, 0.0], [1.0, 1.0])
+    # bins (window [-1, 2), W = 3): -0.5 -> 0; 0, 0.25, 0.999 -> 1; 1.0 -> 2
+    assert list(c[0, 0]) == [0, 0 + 64 + 255, 255]
+    assert list(c[1, 0]) == [128, 384, 128] and list(c[2, 0]) == [128, 384, 128]   # 2-D: blue = 128
+    rgb = O.render_colour(c, 1.0, 1.0)           # radius 1: centre tap only
+    assert rgb[0, 0, 2] == 1.0 and rgb[1, 0, 0] == np.float32(128 / 255)
+
+
 def test_linearity_below_saturation_and_borders():
     rng = np.random.default_rng(3)
     img = rng.integers(0, 3, (1, 20, 30)).astype(np.uint32)
