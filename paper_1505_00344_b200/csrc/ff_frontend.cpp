@@ -731,7 +731,7 @@ struct SignSelect {
 
 }  // namespace
 
-std::string emit_source(const System& s, int sweep_param) {
+std::string emit_source(const System& s, int sweep_param, int kernel_select) {
   if (sweep_param < -1 || sweep_param >= (int)s.param_names.size())
     throw Error(FF_ERR_INVALID_ARG, "sweep parameter index out of range");
   // pass 1: lower once to find exponentials sharing an affine argument c w + d
@@ -831,6 +831,7 @@ std::string emit_source(const System& s, int sweep_param) {
   pre << "#define FF_MINB_P2_T128 " << minb_p2_t128 << "\n";
   pre << "#define FF_MINB_P4 " << minb_p4 << "\n";
   pre << "#define FF_SWEEP " << sweep_param << "\n";
+  pre << "#define FF_KSEL " << kernel_select << "\n";
 
   std::string tmpl(kDeviceTemplate);
   const std::string marker = "#include_generated_rhs";

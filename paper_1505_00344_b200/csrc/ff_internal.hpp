@@ -52,7 +52,9 @@ System parse_system(const ff_system* sys);
 
 // Emit the complete NVRTC source (generated prefix + device template) for the system with
 // parameter `sweep_param` (or -1) per-particle.
-std::string emit_source(const System& s, int sweep_param);
+// kernel_select: which kernels the program defines (FF_KSEL in ff_device.cuh: 0-11 one step variant,
+// 100 = init + render, 255 = all).
+std::string emit_source(const System& s, int sweep_param, int kernel_select = 255);
 
 // NVRTC: source -> sm_100a CUBIN (throws Error(FF_ERR_COMPILE) with the log).
 std::vector<char> compile_cubin(const std::string& source, const std::string& name);

@@ -33,13 +33,17 @@ void ck(cudaError_t e, const char* what) {
   }
 }
 
+// Kernels of one system variant (swept parameter index). Each kernel is its own NVRTC program and
+// library, compiled on first use (FF_KSEL in ff_device.cuh), so a system only pays for what it runs.
 struct Module {
-  cudaLibrary_t lib = nullptr;
+  cudaLibrary_t base_lib = nullptr;  // ff_init + ff_render
   cudaKernel_t init = nullptr;
   cudaKernel_t render = nullptr;
-  // step kernels by (ppt, tpb): 0 p1t128, 1 p1t256, 2 p1t512, 3 p2t128, 4 p2t256, 5 p4t128
-  cudaKernel_t step[6] = {};
-  int occ[6] = {};
+  // step kernels by (ppt, tpb): 0 p1t128, 1 p1t256, 2 p1t512, 3 p2t128, 4 p2t256, 5 p4t128;
+  // +6 = the same with position-linear colour compiled in (ff_project_colour)
+  cudaLibrary_t step_lib[12] = {};
+  cudaKernel_t step[12] = {};
+  int occ[12] = {};
 };
 
 constexpr int kNumStep = 6;
@@ -104,8 +108,11 @@ struct ff_ctx {
   uint64_t tile_base = 0;
 
   ~ff_ctx() {
-    for (auto& m : modules)
-      if (m.second.lib) cudaLibraryUnload(m.second.lib);
+    for (auto& m : modules) {
+      if (m.second.base_lib) cudaLibraryUnload(m.second.base_lib);
+      for (cudaLibrary_t l : m.second.step_lib)
+        if (l) cudaLibraryUnload(l);
+    }
     free_reset_buffers();
     if (tile_ctr) cudaFree(tile_ctr);
   }
@@ -142,23 +149,39 @@ struct ff_ctx {
     ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize");  // host buffers go out of scope
   }
 
+  cudaLibrary_t load(int sweep, int ksel) {
+    std::vector<char> cubin = ff::compile_cubin(ff::emit_source(sys, sweep, ksel), "fireflies_system.cu");
+    cudaLibrary_t lib = nullptr;
+    ck(cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
+    return lib;
+  }
+
+  // init + render kernels of the variant (compiled at first use of the variant)
   Module& module(int sweep) {
     auto it = modules.find(sweep);
     if (it != modules.end()) return it->second;
-    std::string src = ff::emit_source(sys, sweep);
-    std::vector<char> cubin = ff::compile_cubin(src, "fireflies_system.cu");
     Module m;
-    ck(cudaLibraryLoadData(&m.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
-    ck(cudaLibraryGetKernel(&m.init, m.lib, "ff_init"), "cudaLibraryGetKernel(ff_init)");
-    ck(cudaLibraryGetKernel(&m.render, m.lib, "ff_render"), "cudaLibraryGetKernel(ff_render)");
-    for (int i = 0; i < kNumStep; ++i) {
-      ck(cudaLibraryGetKernel(&m.step[i], m.lib, kStepNames[i]), "cudaLibraryGetKernel(ff_step)");
-      int occ = 0;
-      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m.step[i], kStepTPB[i], 0);
-      if (e != cudaSuccess) { cudaGetLastError(); occ = 1; }
-      m.occ[i] = occ > 0 ? occ : 1;
-    }
+    m.base_lib = load(sweep, 100);
+    ck(cudaLibraryGetKernel(&m.init, m.base_lib, "ff_init"), "cudaLibraryGetKernel(ff_init)");
+    ck(cudaLibraryGetKernel(&m.render, m.base_lib, "ff_render"), "cudaLibraryGetKernel(ff_render)");
     return modules.emplace(sweep, m).first->second;
+  }
+
+  // step kernel `id` (0-11) of the variant, compiled at its first launch
+  cudaKernel_t step_kernel(Module& m, int sweep, int id) {
+    if (!m.step[id]) {
+      m.step_lib[id] = load(sweep, id);
+      const std::string name = std::string(kStepNames[id % kNumStep]) + (id >= kNumStep ? "_c" : "");
+      ck(cudaLibraryGetKernel(&m.step[id], m.step_lib[id], name.c_str()), "cudaLibraryGetKernel(ff_step)");
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m.step[id], kStepTPB[id % kNumStep], 0) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        occ = 1;
+      }
+      m.occ[id] = occ > 0 ? occ : 1;
+    }
+    return m.step[id];
   }
 
   int find_param(const char* name) const {
@@ -254,10 +277,13 @@ struct ff_ctx {
     const int64_t ntiles = next_slot / tile;
     if (ntiles == 0) return;
     // position-linear colour: 3 extra per-block table planes in dynamic shared memory
-    const size_t dyn_smem = (image && colour_img) ? 3 * 1024 * sizeof(uint32_t) : 0;
-    int occ = m.occ[si];
-    if (dyn_smem) {
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m.step[si], t, dyn_smem) != cudaSuccess) {
+    const bool colour = image && colour_img;
+    const size_t dyn_smem = colour ? 3 * 1024 * sizeof(uint32_t) : 0;
+    const int kid = si + (colour ? kNumStep : 0);
+    const cudaKernel_t kern = step_kernel(m, sweep_param, kid);
+    int occ = m.occ[kid];
+    if (colour) {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)kern, t, dyn_smem) != cudaSuccess) {
         cudaGetLastError();
         occ = 1;
       }
@@ -266,7 +292,7 @@ struct ff_ctx {
     const int64_t resident = (int64_t)nsm * occ;
     const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
     void* args[] = {&a};
-    ck(cudaLaunchKernel((const void*)m.step[si], dim3(grid), dim3(t), args, dyn_smem, stream), "launch ff_step");
+    ck(cudaLaunchKernel((const void*)kern, dim3(grid), dim3(t), args, dyn_smem, stream), "launch ff_step");
     tile_base += (uint64_t)ntiles + grid;  // each block fetches until it sees a tile >= ntiles
     ++launches;
   }

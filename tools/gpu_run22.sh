@@ -1,0 +1,2 @@
+timeout 1500 python -m pytest tests -m gpu -q -rf 2>&1 | tail -5
+timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['roofline']['frac'])"
