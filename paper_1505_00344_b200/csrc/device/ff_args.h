@@ -25,7 +25,7 @@ struct FFGroup {
   ff_i64 first_global;  // group-global index of the first local particle
   ff_i64 n_global;      // particles in the whole group (all shards)
   ff_u64 sweep_seed;
-  float h, h2, h3, h6;  // signed step direction*dt and h/2, h/3, h/6
+  float h, h2, h6, pad0_;  // signed step direction*dt, h/2, h/6
   float sw_lo, sw_hi, sw_top, sw_val;  // sweep range, largest float below hi, uniform value
   int sweep_mode;       // -1: every particle uses sw_val; 0: Philox-uniform; 1: linspace
   int colour;           // image channel

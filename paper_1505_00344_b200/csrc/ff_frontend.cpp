@@ -251,7 +251,7 @@ namespace {
 enum class K {
   Num, Var, Param, Sweep,
   Neg, Add, Sub, Mul, Rcp, Div,
-  Exp2, Log, Sin, Cos, Tan, Tanh, Sqrt, Abs, Min, Max, Pow, Sigmoid2, Vtrap,
+  Exp2, Log, Sin, Cos, Tan, Tanh, Sqrt, Abs, Min, Max, Pow, Sigmoid2,
   SelAbsLt  // |a0| < value ? a1 : a2 (branch-free select)
 };
 
@@ -665,7 +665,6 @@ struct SignSelect {
       case K::Max: return "ff_max(" + A(0) + ", " + A(1) + ")";
       case K::Pow: return "ff_pow(" + A(0) + ", " + A(1) + ")";
       case K::Sigmoid2: return "ff_rcp(1.0f + ff_exp2(" + A(0) + "))";
-      case K::Vtrap: return "ff_vtrap(" + A(0) + ", " + A(1) + ", " + A(2) + ")";
       case K::SelAbsLt: return "ff_sel_abs_lt(" + A(0) + ", " + A(1) + ", " + A(2) + ", " + flit(n.value) + ")";
       default: throw Error(FF_ERR_COMPILE, "internal: unexpected node in expr()");
     }
@@ -722,7 +721,6 @@ struct SignSelect {
       case K::Tan: n_mufu += 3; break;
       case K::Pow: n_mufu += 2; ++n_arith; break;
       case K::Sigmoid2: n_mufu += 2; ++n_arith; break;
-      case K::Vtrap: n_mufu += 2; n_arith += 9; break;
       case K::SelAbsLt: n_arith += 2; break;
       default: ++n_arith;
     }

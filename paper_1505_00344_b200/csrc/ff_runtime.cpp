@@ -262,7 +262,6 @@ struct ff_ctx {
       const float h = (float)G.dir * dt;
       g.h = h;
       g.h2 = h * 0.5f;
-      g.h3 = h / 3.0f;
       g.h6 = h / 6.0f;
       g.colour = G.colour;
       g.sweep_mode = (sweep_param >= 0) ? G.sweep_mode : -1;
