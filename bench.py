@@ -187,7 +187,10 @@ def run_ours(args, w, rank, world, device):
     with ClockSampler(device.index) as clk:
         t_wall = time.perf_counter()
         for i in range(args.steps):
-            torch.sum(flush, dim=0, out=flush_sink)    # L2 flush between timed iterations (not timed)
+            if args.flush == "read":
+                torch.sum(flush, dim=0, out=flush_sink)    # L2 flush between timed iterations (not timed)
+            elif args.flush == "memset":
+                flush.zero_()
             ev[i][0].record(stream)
             img.zero_()
             ev[i][1].record(stream)
@@ -318,6 +321,8 @@ def main():
     ap.add_argument("--tpb", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-image", action="store_true", help="do not bind the image (integration only)")
+    ap.add_argument("--flush", default="read", choices=["read", "memset", "none"],
+                    help="L2 flush between timed frames (default: read 256 MiB; 'none' only for experiments)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
