@@ -191,7 +191,8 @@ ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view
 /* Advance every particle of every group by n_steps RK4 steps of signed size direction*dt
  * (dt may be negative), then, if an image is bound, bin every particle once
  * (fused). One kernel launch; async. n_steps >= 0 (0 = bin only).
- * Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE (no groups), FF_ERR_CUDA. */
+ * The first launch of a kernel variant compiles it (NVRTC, ~0.5 s; cached per process).
+ * Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE (no groups), FF_ERR_COMPILE, FF_ERR_CUDA. */
 ff_status ff_step(ff_ctx* ctx, int64_t n_steps, float dt);
 
 /* Device-side reset (trajectories that leave the region, or have not been reset for
