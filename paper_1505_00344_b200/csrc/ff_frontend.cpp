@@ -366,6 +366,16 @@ struct Dag {
       if (ny.k == K::Mul && nodes[ny.a[0]].uniform) return mul(mul(x, ny.a[0]), ny.a[1]);
       // u * (-w) -> (-u) * w
       if (ny.k == K::Neg) return mul(neg(x), ny.a[0]);
+      // u * (a / b) -> (u a) / b: u a often folds (e.g. into an existing affine node)
+      if (ny.k == K::Div) return div(mul(x, ny.a[0]), ny.a[1]);
+      // u * select(c, a, b) -> select(c, u a, u b): the constant folds into both branches
+      if (ny.k == K::SelAbsLt) {
+        DNode sn;
+        sn.k = K::SelAbsLt;
+        sn.value = ny.value;
+        sn.a = {ny.a[0], mul(x, ny.a[1]), mul(x, ny.a[2])};
+        return intern(sn);
+      }
       // u * (w +- v) with one uniform term -> distribute: one FFMA instead of FADD + FMUL
       if (ny.k == K::Add || ny.k == K::Sub) {
         const int p = ny.a[0], q = ny.a[1];
@@ -498,11 +508,12 @@ struct Dag {
         if (f == "vtrap") {
           // x / (exp(x/y) - 1), and for |x/y| < 0.1 the series y (1 - u/2 + u^2/12 - u^4/720)
           // (reading R10); lowered to primitives so its exponential can be shared (exp_)
+          // Horner: y (1 - u/2 + u^2 (1/12 - u^2/720)) -- 5 FMA-pipe ops for the rarely used branch
           const int u = mul(x, rcp(y));
           const int dir = div(x, sub(exp_(u), N(1.0)));
           const int u2 = mul(u, u);
-          const int ser = mul(y, sub(add(sub(N(1.0), mul(N(0.5), u)), mul(N(1.0 / 12.0), u2)),
-                                     mul(N(1.0 / 720.0), mul(u2, u2))));
+          const int inner = add(mul(N(-1.0 / 720.0), u2), N(1.0 / 12.0));
+          const int ser = mul(y, add(mul(inner, u2), add(mul(N(-0.5), u), N(1.0))));
           DNode sn;
           sn.k = K::SelAbsLt;
           sn.value = 0.1;
@@ -540,7 +551,7 @@ struct Choice { enum Form { ADD, SUB, FMA, MUL, DIV, OTHER, NEGATE } form; Opera
 struct SignSelect {
   const Dag& g;
   const std::vector<char>& live;
-  std::vector<int> uses;
+  std::vector<int> uses, addsub_uses;
   std::vector<double> c[2];
   std::map<std::pair<int, int>, std::string> memo;
   std::vector<std::string> uref;
@@ -551,9 +562,13 @@ struct SignSelect {
       : g(dag), live(lv), uses(dag.nodes.size(), 0), uref(dag.nodes.size()) {
     c[0].assign(g.nodes.size(), 0.0);
     c[1].assign(g.nodes.size(), 0.0);
+    addsub_uses.assign(g.nodes.size(), 0);
     for (size_t id = 0; id < g.nodes.size(); ++id)
       if (live[id])
-        for (int a : g.nodes[id].a) ++uses[a];
+        for (int a : g.nodes[id].a) {
+          ++uses[a];
+          if (g.nodes[id].k == K::Add || g.nodes[id].k == K::Sub) ++addsub_uses[a];
+        }
     for (int r : roots) ++uses[r];
     for (size_t id = 0; id < g.nodes.size(); ++id) {
       if (!live[id]) continue;
@@ -564,9 +579,11 @@ struct SignSelect {
   }
 
   double cost(int id, int s) const { return c[s][id]; }
+  // a varying product whose every use is an addition / subtraction: each user absorbs it into an
+  // FFMA (duplicating the multiply costs nothing), so it is never materialised on its own
   bool fusable(int id) const {
     const DNode& n = g.nodes[id];
-    return n.k == K::Mul && !n.uniform && uses[id] == 1;
+    return n.k == K::Mul && !n.uniform && uses[id] == addsub_uses[id];
   }
   // cheapest factor signs (sx, sy) with sx xor sy = s for the product node m
   double prod(int m, int s, Operand& x, Operand& y) const {
