@@ -159,7 +159,12 @@ def run_ours(args, w, rank, world, device):
     if w.get("prerun"):
         ctx.step(w["prerun"], w["dt"])
     axes, view = projection(w)
-    img = ctx.project(axes, view, w["W"], w["H"], w["C"])
+    fused = args.exchange == "fused" and not args.no_image
+    if fused:   # the image sum over ranks happens inside ff_step (ff_set_exchange), no NCCL call
+        from paper_1505_00344_b200 import dist as ffdist
+        img = ffdist.bind_exchanged_image(ctx, axes, view, w["W"], w["H"], w["C"])
+    else:
+        img = ctx.project(axes, view, w["W"], w["H"], w["C"])
     if args.no_image:   # integration only (HBM roofline of single-step launches without binning)
         ctx.unbind_image()
     n_local = sum(ctx.group_info(g)[1] for g in gids)
@@ -169,11 +174,12 @@ def run_ours(args, w, rank, world, device):
     flush = torch.ones(64 << 20, dtype=torch.float32, device=device)
     flush_sink = torch.empty((), dtype=torch.float32, device=device)
     dist = world > 1
+    reduce = dist and not fused
 
     def frame():
         img.zero_()
         ctx.step(S, w["dt"])
-        if dist:
+        if reduce:
             torch.distributed.all_reduce(img)
 
     for _ in range(args.warmup):
@@ -196,7 +202,7 @@ def run_ours(args, w, rank, world, device):
             ev[i][1].record(stream)
             ctx.step(S, w["dt"])
             ev[i][2].record(stream)
-            if dist:
+            if reduce:
                 torch.distributed.all_reduce(img)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
@@ -231,7 +237,7 @@ def run_ours(args, w, rank, world, device):
                 F.check(F.lib().ff_write_state(ctx.ctx, g, 0, t.shape[1], F.C.c_void_p(t.data_ptr())))
             img.zero_()
             ctx.step(S, w["dt"])
-            if dist:
+            if reduce:
                 torch.distributed.all_reduce(img)
             F.ff_read_image_into(ctx.ctx, host_img.data_ptr())
 
@@ -255,7 +261,7 @@ def run_ours(args, w, rank, world, device):
         e2e = {"value": n_total * S / (ms * 1e-3), "unit": "particle-steps/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ms,
                "path": "per frame: ff_write_state (pinned host -> device, whole state), ff_step, "
-                       + ("NCCL image all-reduce, " if dist else "") + "ff_read_image (device -> pinned host)"}
+                       + ("NCCL image all-reduce, " if reduce else "") + "ff_read_image (device -> pinned host)"}
     im_sum = int(img.sum().item())
     ctx.close()
     sweep_idx = -1
@@ -324,6 +330,9 @@ def main():
     ap.add_argument("--flush", default="read", choices=["read", "memset", "none"],
                     help="L2 flush between timed frames (default: read 256 MiB; 'none' only for experiments)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
+                    help="per-frame image sum over ranks: NCCL all-reduce after the launch, or fused into "
+                         "the launch over peer memory (ff_set_exchange)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = WORKLOADS[args.config]
@@ -334,8 +343,10 @@ def main():
     config = {"workload": args.config, "description": w["desc"], "steps_per_frame": S, "dt": w["dt"],
               "particles_per_gpu": (sum(g[0] for g in w["groups"]) // (world if w.get("strong") else 1)),
               "image": [w["C"], w["H"], w["W"]], "l2": "flushed between timed frames (256 MiB read, outside the timed events)",
-              "parallelism": f"particles sharded over {world} GPU(s), NCCL image all-reduce per frame"
-              if world > 1 else "1 GPU"}
+              "parallelism": (f"particles sharded over {world} GPU(s), " + (
+                  "image sum fused into the step launch over NVLink peer memory" if args.exchange == "fused"
+                  else "NCCL image all-reduce per frame")) if world > 1 else "1 GPU",
+              "exchange": args.exchange}
 
     if args.impl == "reference":
         if rank != 0:

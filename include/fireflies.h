@@ -37,6 +37,7 @@ extern "C" {
 #define FF_MAX_PARAMS 128  /* parameters per system */
 #define FF_MAX_GROUPS 16   /* particle groups per context */
 #define FF_TILE 512        /* group slot ranges are padded to a multiple of this */
+#define FF_MAX_PEERS 8     /* ranks in one fused image exchange (one node) */
 
 typedef enum {
   FF_OK = 0,
@@ -250,8 +251,42 @@ ff_status ff_project_colour(ff_ctx* ctx, const float* lo, const float* hi, uint3
 /* Number of kernel launches this context has issued (for bench evidence). */
 ff_status ff_launch_count(ff_ctx* ctx, int64_t* count);
 
-/* Synchronise the bound stream; surfaces asynchronous kernel errors as FF_ERR_CUDA. */
+/* Synchronise the bound stream; surfaces asynchronous kernel errors as FF_ERR_CUDA, including an
+ * image exchange that timed out waiting for a peer (ff_set_exchange). */
 ff_status ff_sync(ff_ctx* ctx);
+
+/* Image exchange over peer memory: the path's one exchange step -- the
+ * sum of the per-rank density images of a sharded run (PAPER.md:236 additive blending over all
+ * particles) -- done by the library on the step's stream, over NVLink / NVSwitch peer memory, instead
+ * of a separate all-reduce. After this call every binning launch of this context (ff_step,
+ * ff_project's immediate binning) is followed, in stream order, by an exchange kernel: a barrier over
+ * the `world` ranks (their histograms are complete), then rank r sums pixel slice r (16-byte units,
+ * split evenly; the C*H*W % 4 tail words belong to rank world-1) over all ranks' images and stores the
+ * sum into every rank's image, then a second barrier. When it completes, the bound image equals the
+ * element-wise sum over ranks of the images each rank's launch produced alone -- bit-exact, integer
+ * -- i.e. ff_step followed by an all-reduce (previous contents included: zero the image per frame).
+ *   peer_images[p]   DEVICE pointer, valid in THIS process, to rank p's bound uint32 [C][H][W] image
+ *                    (16-byte aligned; peer_images[rank] must be the image bound here with ff_project;
+ *                    all ranks bind the same C, H, W). Typically symmetric memory mapped over
+ *                    NVLink (torch symmetric memory, CUDA IPC) or, on one GPU, other contexts'.
+ *   peer_signals[p]  DEVICE pointer to rank p's FF_MAX_PEERS uint64 signal words (8-byte aligned),
+ *                    zeroed on every rank before the first exchanged launch; written only by the
+ *                    library (rank q stores barrier values into word q of every rank's array).
+ *   timeout_ms       bound on every wait inside the exchange; a peer that does not arrive in time
+ *                    makes the launch finish with an incomplete image and ff_sync report FF_ERR_CUDA.
+ * Collective: every rank calls it with the same world and tables (its own rank), no exchanged
+ * launch in flight, and then issues the same sequence of binning launches. world = 0 (tables
+ * ignored) turns the exchange off; so does binding another image with ff_project. Position-colour
+ * images are not exchanged (FF_ERR_STATE).
+ * Errors: FF_ERR_INVALID_ARG (ranges, NULL / misaligned pointers, peer_images[rank] != image),
+ * FF_ERR_STATE (no image bound, colour image bound), FF_ERR_CUDA. */
+ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* peer_images,
+                          uint64_t* const* peer_signals, double timeout_ms);
+
+/* Upper bound on the blocks of every step and exchange launch (0 = the default: every resident block
+ * for a step, 2 per SM for an exchange). For several ranks sharing one GPU (their exchanges must run
+ * concurrently), and for tuning. Errors: FF_ERR_INVALID_ARG. */
+ff_status ff_set_grid_limit(ff_ctx* ctx, int max_blocks);
 
 #ifdef __cplusplus
 }

@@ -17,13 +17,15 @@ FF_TILE = 512
 FF_MAX_DIM = 64
 FF_MAX_PARAMS = 128
 FF_MAX_GROUPS = 16
+FF_MAX_PEERS = 8
 
 # Every symbol include/fireflies.h declares (checked by tests/test_abi.py).
 EXPORTS = ["ff_last_error", "ff_abi_version", "ff_build_info", "ff_emit_source", "ff_compile_cubin", "ff_create", "ff_destroy",
            "ff_set_stream", "ff_set_shard", "ff_shard_range", "ff_bind_state", "ff_group_slots", "ff_init_group", "ff_group_info",
            "ff_set_param", "ff_get_param", "ff_sweep_param", "ff_project", "ff_step", "ff_set_reset",
            "ff_read_epochs", "ff_set_launch",
-           "ff_read_state", "ff_write_state", "ff_read_image", "ff_render", "ff_project_colour", "ff_launch_count", "ff_sync"]
+           "ff_read_state", "ff_write_state", "ff_read_image", "ff_render", "ff_project_colour", "ff_launch_count", "ff_sync",
+           "ff_set_exchange", "ff_set_grid_limit"]
 
 
 class FFError(RuntimeError):
@@ -82,6 +84,8 @@ def lib():
             "ff_project_colour": ([P, P, P, P], C.c_int),
             "ff_launch_count": ([P, C.POINTER(i64)], C.c_int),
             "ff_sync": ([P], C.c_int),
+            "ff_set_exchange": ([P, i32, i32, P, P, C.c_double], C.c_int),
+            "ff_set_grid_limit": ([P, i32], C.c_int),
         }
         assert set(sig) == set(EXPORTS)
         for name, (args, res) in sig.items():

@@ -14,6 +14,12 @@ typedef unsigned int ff_u32;
 
 #define FF_MAX_GROUPS_ 16
 #define FF_MAX_DIM_ 64
+#define FF_MAX_PEERS_ 8
+// word offsets in the exchange sync block (each word on its own 128-byte line)
+#define FF_XS_ARRIVE 0
+#define FF_XS_GO 16
+#define FF_XS_TIMEOUT 32
+#define FF_XS_WORDS 48
 #ifndef FF_NP_ALLOC
 #define FF_NP_ALLOC 128  /* host side: FF_MAX_PARAMS; device side: the system's count */
 #endif
@@ -64,6 +70,20 @@ struct FFStepArgs {
   float bound_lo[FF_MAX_DIM_], bound_hi[FF_MAX_DIM_];
   FFGroup g[FF_MAX_GROUPS_];
   float p[FF_NP_ALLOC]; // parameter values (must stay the last member)
+};
+
+// Image exchange (NEXT row 2): launched right after a binning step launch of an
+// exchanging context (ff_set_exchange); sums the bound images of all ranks over peer memory, each
+// rank owning one slice of the pixels, in place.
+struct FFXchgArgs {
+  ff_u32* img[FF_MAX_PEERS_];   // every rank's bound image, as mapped in this process; [rank] = own
+  ff_u64* sig[FF_MAX_PEERS_];   // every rank's signal words [FF_MAX_PEERS_] (written by the peers)
+  ff_u64* sync;                 // library-owned sync block (FF_XS_* word offsets)
+  ff_u64 words;                 // C * H * W
+  ff_u64 bar_base;              // arrival tickets taken before this launch
+  ff_u64 seq;                   // exchanges before this one: barrier values 2 seq + 1, 2 seq + 2
+  ff_u64 timeout_ns;            // bound on every wait (a missing peer cannot hang the GPU)
+  int rank, world;
 };
 
 // Render post-process (NEXT row 3): count image -> RGB with sprite falloff.

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstddef>
 #include <cstring>
 #include <map>
@@ -19,6 +20,7 @@
 
 static_assert(sizeof(FFGroup) == 104, "FFGroup layout");
 static_assert(offsetof(FFStepArgs, g) == 744, "FFStepArgs layout");
+static_assert(FF_MAX_PEERS_ == FF_MAX_PEERS, "peer table size");
 static_assert(FF_MAX_DIM_ == FF_MAX_DIM, "bounds table size");
 static_assert(FF_MAX_GROUPS_ == FF_MAX_GROUPS, "group table size");
 
@@ -40,13 +42,17 @@ struct Module {
   cudaKernel_t init = nullptr;
   cudaKernel_t render = nullptr;
   // step kernels by (ppt, tpb): 0 p1t128, 1 p1t256, 2 p1t512, 3 p2t128, 4 p2t256, 5 p4t128;
-  // +6 = the same with position-linear colour compiled in (ff_project_colour)
+  // +6 = the same with position-linear colour compiled in (ff_project_colour), +12 = with the fused
+  // image exchange (ff_set_exchange)
+  cudaKernel_t exchange = nullptr;  // (in base_lib)
   cudaLibrary_t step_lib[12] = {};
   cudaKernel_t step[12] = {};
   int occ[12] = {};
 };
 
 constexpr int kNumStep = 6;
+constexpr int kSyncWords = 16 + FF_XS_WORDS;
+  // tile counter line + the exchange sync block
 int step_index(int ppt, int tpb) {
   if (ppt == 1) return tpb == 128 ? 0 : tpb == 256 ? 1 : tpb == 512 ? 2 : -1;
   if (ppt == 2) return tpb == 128 ? 3 : tpb == 256 ? 4 : -1;
@@ -104,8 +110,16 @@ struct ff_ctx {
   float* ic_box = nullptr;
   std::vector<double> t_elapsed;  // per group: simulated time since creation (sum of |dt| n)
   // dynamic tile scheduler counter (library-owned, 8 bytes) and the fetch numbers used so far
+  // [0] tile counter; from word 16 on: the exchange sync block (FF_XS_*, one 128-byte line per word)
   unsigned long long* tile_ctr = nullptr;
   uint64_t tile_base = 0;
+  int grid_limit = 0;  // ff_set_grid_limit (0 = every resident block)
+  // fused image exchange (ff_set_exchange): peer tables, barrier bookkeeping
+  int xrank = 0, xworld = 0;
+  uint32_t* ximg[FF_MAX_PEERS] = {};
+  uint64_t* xsig[FF_MAX_PEERS] = {};
+  uint64_t xbar = 0, xseq = 0, xtimeout_ns = 0;
+  bool xused = false;
 
   ~ff_ctx() {
     for (auto& m : modules) {
@@ -164,10 +178,11 @@ struct ff_ctx {
     m.base_lib = load(sweep, 100);
     ck(cudaLibraryGetKernel(&m.init, m.base_lib, "ff_init"), "cudaLibraryGetKernel(ff_init)");
     ck(cudaLibraryGetKernel(&m.render, m.base_lib, "ff_render"), "cudaLibraryGetKernel(ff_render)");
+    ck(cudaLibraryGetKernel(&m.exchange, m.base_lib, "ff_exchange"), "cudaLibraryGetKernel(ff_exchange)");
     return modules.emplace(sweep, m).first->second;
   }
 
-  // step kernel `id` (0-11) of the variant, compiled at its first launch
+  // step kernel `id` (0-17) of the variant, compiled at its first launch
   cudaKernel_t step_kernel(Module& m, int sweep, int id) {
     if (!m.step[id]) {
       m.step_lib[id] = load(sweep, id);
@@ -214,6 +229,10 @@ struct ff_ctx {
   void launch_step(int64_t n_steps, float dt) {
     if (groups.empty()) throw ff::Error(FF_ERR_STATE, "no particle groups");
     if (!std::isfinite(dt)) throw ff::Error(FF_ERR_INVALID_ARG, "dt is not finite");
+    if (xworld) {
+      if (image != ximg[xrank]) throw ff::Error(FF_ERR_STATE, "exchange: the bound image is not this rank's peer image");
+      if (colour_img) throw ff::Error(FF_ERR_STATE, "exchange: position colour images are not exchanged");
+    }
     int p, t;
     default_launch(p, t, n_steps);
     const int si = step_index(p, t);
@@ -276,7 +295,10 @@ struct ff_ctx {
     for (size_t k = 0; k < params.size(); ++k) a.p[k] = params[k];
     const int64_t tile = (int64_t)p * t;
     const int64_t ntiles = next_slot / tile;
-    if (ntiles == 0) return;
+    if (ntiles == 0) {
+      if (xworld) launch_exchange(m);  // this rank has no particles; its peers still wait for it
+      return;
+    }
     // position-linear colour: 3 extra per-block table planes in dynamic shared memory
     const bool colour = image && colour_img;
     const size_t dyn_smem = colour ? 3 * 1024 * sizeof(uint32_t) : 0;
@@ -290,11 +312,39 @@ struct ff_ctx {
       }
       occ = occ > 0 ? occ : 1;
     }
-    const int64_t resident = (int64_t)nsm * occ;
+    int64_t resident = (int64_t)nsm * occ;
+    if (grid_limit > 0 && grid_limit < resident) resident = grid_limit;
     const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
     void* args[] = {&a};
     ck(cudaLaunchKernel((const void*)kern, dim3(grid), dim3(t), args, dyn_smem, stream), "launch ff_step");
     tile_base += (uint64_t)ntiles + grid;  // each block fetches until it sees a tile >= ntiles
+    ++launches;
+    if (xworld && image) launch_exchange(m);
+  }
+
+  // the image exchange after a binning launch (ff_set_exchange; ff_device.cuh "image exchange")
+  void launch_exchange(Module& m) {
+    FFXchgArgs x;
+    std::memset(&x, 0, sizeof x);
+    for (int p = 0; p < xworld; ++p) {
+      x.img[p] = ximg[p];
+      x.sig[p] = reinterpret_cast<ff_u64*>(xsig[p]);
+    }
+    x.sync = reinterpret_cast<ff_u64*>(tile_ctr) + 16;
+    x.words = (ff_u64)W * (ff_u64)H * (ff_u64)C;
+    x.bar_base = xbar;
+    x.seq = xseq;
+    x.timeout_ns = xtimeout_ns;
+    x.rank = xrank;
+    x.world = xworld;
+    // 2 blocks of 256 threads per SM (fewer if ff_set_grid_limit says so): enough loads in flight
+    unsigned grid = (unsigned)(2 * nsm);
+    if (grid_limit > 0 && (unsigned)grid_limit < grid) grid = (unsigned)grid_limit;
+    void* args[] = {&x};
+    ck(cudaLaunchKernel((const void*)m.exchange, dim3(grid), dim3(256), args, 0, stream), "launch ff_exchange");
+    xbar += grid;
+    ++xseq;
+    xused = true;
     ++launches;
   }
 };
@@ -383,8 +433,8 @@ ff_status ff_create(const ff_system* sys, int device, ff_ctx** out) {
     c->device = device;
     ck(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
     c->module(-1);
-    ck(cudaMalloc(&c->tile_ctr, sizeof(unsigned long long)), "cudaMalloc tile counter");
-    ck(cudaMemset(c->tile_ctr, 0, sizeof(unsigned long long)), "cudaMemset tile counter");
+    ck(cudaMalloc(&c->tile_ctr, kSyncWords * sizeof(unsigned long long)), "cudaMalloc tile counter");
+    ck(cudaMemset(c->tile_ctr, 0, kSyncWords * sizeof(unsigned long long)), "cudaMemset tile counter");
   } catch (...) {
     delete c;
     throw;
@@ -611,6 +661,7 @@ ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view
     ctx->image = nullptr;
     ctx->colour_img = nullptr;
     ctx->proj = 0;
+    ctx->xworld = 0;
     return FF_OK;
   }
   need(axes && view, FF_ERR_INVALID_ARG, "axes / view is NULL");
@@ -642,6 +693,7 @@ ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view
   ctx->H = H;
   ctx->C = C;
   ctx->image = image;
+  ctx->xworld = 0;  // (re)binding an image ends an exchange (ff_set_exchange again)
   if (!ctx->groups.empty()) ctx->launch_step(0, 0.0f);
   FF_CATCH
 }
@@ -785,6 +837,68 @@ ff_status ff_sync(ff_ctx* ctx) {
   need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
   ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
   ck(cudaGetLastError(), "kernel error");
+  if (ctx->xused) {
+    unsigned long long flag = 0;
+    unsigned long long* f = ctx->tile_ctr + 16 + FF_XS_TIMEOUT;
+    ck(cudaMemcpy(&flag, f, sizeof flag, cudaMemcpyDeviceToHost), "cudaMemcpy exchange flag");
+    if (flag) {
+      ck(cudaMemset(f, 0, sizeof flag), "cudaMemset exchange flag");
+      throw ff::Error(FF_ERR_CUDA, "image exchange timed out waiting for a peer (the image of that launch is incomplete)");
+    }
+  }
+  FF_CATCH
+}
+
+ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* peer_images,
+                          uint64_t* const* peer_signals, double timeout_ms) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  if (world == 0) {
+    ctx->xworld = 0;
+    return FF_OK;
+  }
+  need(world >= 1 && world <= FF_MAX_PEERS && rank >= 0 && rank < world, FF_ERR_INVALID_ARG,
+       "need 1 <= world <= FF_MAX_PEERS and 0 <= rank < world");
+  need(peer_images && peer_signals, FF_ERR_INVALID_ARG, "peer tables are NULL");
+  need(timeout_ms > 0.0 && timeout_ms <= 3.6e6, FF_ERR_INVALID_ARG, "timeout_ms must be in (0, 3.6e6]");
+  need(ctx->image != nullptr, FF_ERR_STATE, "bind this rank's image with ff_project first");
+  need(ctx->colour_img == nullptr, FF_ERR_STATE, "position colour images are not exchanged");
+  need(peer_images[rank] == ctx->image, FF_ERR_INVALID_ARG, "peer_images[rank] must be the bound image");
+  for (int p = 0; p < world; ++p) {
+    need(peer_images[p] && ((uintptr_t)peer_images[p] & 15) == 0, FF_ERR_INVALID_ARG,
+         "peer images must be non-NULL and 16-byte aligned");
+    need(peer_signals[p] && ((uintptr_t)peer_signals[p] & 7) == 0, FF_ERR_INVALID_ARG,
+         "peer signals must be non-NULL and 8-byte aligned");
+  }
+  for (int p = 0; p < FF_MAX_PEERS; ++p) {
+    ctx->ximg[p] = p < world ? peer_images[p] : nullptr;
+    ctx->xsig[p] = p < world ? peer_signals[p] : nullptr;
+  }
+  // a new exchange starts its barrier values at 1 again: clear the go flag (signals are the caller's)
+  ck(cudaMemsetAsync(ctx->tile_ctr + 16 + FF_XS_GO, 0, sizeof(unsigned long long), ctx->stream),
+     "cudaMemsetAsync go flag");
+  ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+  // compile / load the step kernel now: no NVRTC or module load between the ranks' first launches
+  int pp, tt;
+  ctx->default_launch(pp, tt);
+  Module& m = ctx->module(ctx->sweep_param);
+  ctx->step_kernel(m, ctx->sweep_param, step_index(pp, tt));
+  // and force the (lazily loaded) exchange kernel in now: a lazy load at its first launch can wait
+  // for the device while a peer's exchange kernel spins waiting for this rank (deadlock on one GPU)
+  cudaFuncAttributes fa;
+  ck(cudaFuncGetAttributes(&fa, (const void*)m.exchange), "cudaFuncGetAttributes(ff_exchange)");
+  ctx->xrank = rank;
+  ctx->xworld = world;
+  ctx->xseq = 0;
+  ctx->xtimeout_ns = (uint64_t)(timeout_ms * 1e6);
+  FF_CATCH
+}
+
+ff_status ff_set_grid_limit(ff_ctx* ctx, int max_blocks) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  need(max_blocks >= 0, FF_ERR_INVALID_ARG, "max_blocks must be >= 0");
+  ctx->grid_limit = max_blocks;
   FF_CATCH
 }
 

@@ -1,8 +1,10 @@
 """Multi-GPU plumbing: one process per GPU, particles sharded contiguously per group
 (ff_set_shard / ff_shard_range), and the path's one exchange step -- the per-frame sum of the
-int32 density images -- as a torch.distributed all-reduce (NCCL over NVLink/NVSwitch on GPUs, gloo
-on CPU in the tests). Parameters changed on rank 0 are broadcast so every shard integrates the
-same system."""
+int32 density images -- either fused into the step launch over NVLink peer memory
+(bind_exchanged_image -> ff_set_exchange; torch symmetric memory only maps the buffers) or as a
+torch.distributed all-reduce (reduce_image: NCCL over NVLink/NVSwitch on GPUs, gloo on CPU in the
+tests). Parameters changed on rank 0 are broadcast so every shard integrates the same system
+(PAPER.md:242)."""
 import os
 
 import torch
@@ -49,3 +51,53 @@ def broadcast_params(ctx, names, src=0, device=None):
     dist.broadcast(vals, src=src)
     for n, v in zip(names, vals.tolist()):
         ctx.set_param(n, v)
+
+
+FF_MAX_PEERS = 8
+
+
+def exchange_layout(C_, H, W):
+    """Symmetric buffer layout of one rank for the fused exchange, in int32 words: the image
+    [C][H][W] first, then FF_MAX_PEERS uint64 signal words at a 256-byte boundary.
+    Returns (image_words, signal_offset_bytes, total_words)."""
+    words = int(C_) * int(H) * int(W)
+    sig_words = (words + 63) // 64 * 64
+    return words, 4 * sig_words, sig_words + 2 * FF_MAX_PEERS
+
+
+def peer_tables(buffer_ptrs, C_, H, W):
+    """(peer image pointers, peer signal pointers) from every rank's symmetric buffer base address."""
+    _, sig_off, _ = exchange_layout(C_, H, W)
+    return [int(p) for p in buffer_ptrs], [int(p) + sig_off for p in buffer_ptrs]
+
+
+def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=60000.0):
+    """Bind a symmetric-memory image to `ctx` and turn on the fused in-launch image exchange: from
+    now on every ff_step of every rank ends with the image summed over all ranks (no separate
+    collective). Collective over `group` (default: the world); returns the bound image tensor
+    [C][H][W] (int32, zeroed). Needs one GPU per rank with peer access (NVLink / NVSwitch)."""
+    words, sig_off, total = exchange_layout(C_, H, W)
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:   # one rank: its own tables
+        buf = torch.zeros(total, dtype=torch.int32, device=ctx.device)
+        image = buf[:words].view(C_, H, W)
+        ctx.project(axes, view, W, H, C_, image=image)
+        image.zero_()
+        torch.cuda.synchronize(ctx.device)
+        imgs, sigs = peer_tables([buf.data_ptr()], C_, H, W)
+        ctx.set_exchange(0, 1, imgs, sigs, timeout_ms)
+        ctx._symm = (buf,)
+        return image
+    import torch.distributed._symmetric_memory as symm_mem
+    group = group if group is not None else dist.group.WORLD
+    buf = symm_mem.empty(total, dtype=torch.int32, device=ctx.device)
+    buf.zero_()
+    handle = symm_mem.rendezvous(buf, group)
+    image = buf[:words].view(C_, H, W)
+    ctx.project(axes, view, W, H, C_, image=image)   # binds (and bins the current state locally)
+    image.zero_()
+    torch.cuda.synchronize(ctx.device)
+    dist.barrier(group)                                # every rank's signals are zero
+    imgs, sigs = peer_tables(handle.buffer_ptrs, C_, H, W)
+    ctx.set_exchange(handle.rank, handle.world_size, imgs, sigs, timeout_ms)
+    ctx._symm = (buf, handle)                          # keep the mapping alive with the context
+    return image

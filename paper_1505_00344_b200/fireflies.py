@@ -172,6 +172,20 @@ def ff_sync(ctx):
     check(lib().ff_sync(ctx))
 
 
+def ff_set_exchange(ctx, rank: int, world: int, peer_image_ptrs, peer_signal_ptrs, timeout_ms: float = 60000.0):
+    """Fused in-launch image all-reduce over peer memory (world = 0: off). Pointers are ints."""
+    if world == 0:
+        check(lib().ff_set_exchange(ctx, 0, 0, None, None, 1.0))
+        return
+    imgs = (C.c_void_p * world)(*[int(p) for p in peer_image_ptrs])
+    sigs = (C.c_void_p * world)(*[int(p) for p in peer_signal_ptrs])
+    check(lib().ff_set_exchange(ctx, rank, world, imgs, sigs, timeout_ms))
+
+
+def ff_set_grid_limit(ctx, max_blocks: int):
+    check(lib().ff_set_grid_limit(ctx, max_blocks))
+
+
 # ---------------------------------------------------------------- plumbing: Context
 class Context:
     """One system on one CUDA device (torch for memory and the stream).
@@ -294,6 +308,12 @@ class Context:
             out = torch.empty((3, H, W), dtype=torch.float32, device=self.device)
         ff_render(self.ctx, colours, intensity, radius_px, out.data_ptr())
         return out
+
+    def set_exchange(self, rank, world, peer_image_ptrs=(), peer_signal_ptrs=(), timeout_ms=60000.0):
+        ff_set_exchange(self.ctx, rank, world, peer_image_ptrs, peer_signal_ptrs, timeout_ms)
+
+    def set_grid_limit(self, max_blocks):
+        ff_set_grid_limit(self.ctx, max_blocks)
 
     def launch_count(self):
         return ff_launch_count(self.ctx)

@@ -82,3 +82,30 @@ def test_shard_ranges_partition_every_group():
                 assert f0 + c0 == f1
             assert parts[-1][0] + parts[-1][1] == n
             assert max(c for _, c in parts) - min(c for _, c in parts) <= 1
+
+
+def _exchange_worker(rank, world, port, out):
+    """Host side of the fused exchange (bind_exchanged_image): every rank derives identical peer
+    tables from the gathered symmetric-buffer bases (fake addresses here: no GPU)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    from paper_1505_00344_b200 import dist as ffdist
+    ffdist.init_from_env("gloo")
+    bases = [None] * world
+    dist.all_gather_object(bases, 0x7f0000000000 + rank * (1 << 30))
+    out[rank] = ffdist.peer_tables(bases, 2, 29, 37)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_exchange_peer_tables_agree_across_ranks():
+    from paper_1505_00344_b200 import dist as ffdist
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_exchange_worker, args=(world, free_port(), out), nprocs=world, join=True)
+    assert out[0] == out[1]
+    imgs, sigs = out[0]
+    words, sig_off, total = ffdist.exchange_layout(2, 29, 37)
+    for i, s in zip(imgs, sigs):
+        assert i % 256 == 0 and (s - i) == sig_off and sig_off % 256 == 0
+        assert sig_off >= 4 * words and 4 * total - sig_off == 8 * ffdist.FF_MAX_PEERS
