@@ -539,6 +539,41 @@ std::string flit(double v) {
 }
 
 
+template <class F>
+std::string node_expr(const DNode& n, F A) {
+  switch (n.k) {
+    case K::Neg: return "-" + A(0);
+    case K::Add: return A(0) + " + " + A(1);
+    case K::Sub: return A(0) + " - " + A(1);
+    case K::Mul: return A(0) + " * " + A(1);
+    case K::Rcp: return "ff_rcp(" + A(0) + ")";
+    case K::Div: return "ff_div(" + A(0) + ", " + A(1) + ")";
+    case K::Exp2: return "ff_exp2(" + A(0) + ")";
+    case K::Log: return "ff_log(" + A(0) + ")";
+    case K::Sin: return "ff_sin(" + A(0) + ")";
+    case K::Cos: return "ff_cos(" + A(0) + ")";
+    case K::Tan: return "ff_tan(" + A(0) + ")";
+    case K::Tanh: return "ff_tanh(" + A(0) + ")";
+    case K::Sqrt: return "ff_sqrt(" + A(0) + ")";
+    case K::Abs: return "ff_abs(" + A(0) + ")";
+    case K::Min: return "ff_min(" + A(0) + ", " + A(1) + ")";
+    case K::Max: return "ff_max(" + A(0) + ", " + A(1) + ")";
+    case K::Pow: return "ff_pow(" + A(0) + ", " + A(1) + ")";
+    case K::Sigmoid2: return "ff_rcp(1.0f + ff_exp2(" + A(0) + "))";
+    case K::SelAbsLt: return "ff_sel_abs_lt(" + A(0) + ", " + A(1) + ", " + A(2) + ", " + flit(n.value) + ")";
+    default: throw Error(FF_ERR_COMPILE, "internal: unexpected node in expr()");
+  }
+}
+
+
+// inline expression of a uniform (loop-invariant) node, fully parenthesised
+std::string uexpr(const Dag& g, int id) {
+  const DNode& n = g.nodes[id];
+  if (n.k == K::Num) return flit(n.value);
+  if (n.k == K::Param) return "a.p[" + std::to_string(n.index) + "]";
+  return "(" + node_expr(n, [&](int j) { return uexpr(g, n.a[j]); }) + ")";
+}
+
 // ---------------------------------------------------------------- sign-aware instruction selection
 // FFMA2 / FADD2 / FMUL2 (the packed pair path) have no operand negation, so every "-v" of a
 // varying value costs an instruction, while negating a uniform (loop-invariant) value is free. For
@@ -662,30 +697,7 @@ struct SignSelect {
   }
 
   template <class F>
-  std::string expr(const DNode& n, F A) {
-    switch (n.k) {
-      case K::Neg: return "-" + A(0);
-      case K::Add: return A(0) + " + " + A(1);
-      case K::Sub: return A(0) + " - " + A(1);
-      case K::Mul: return A(0) + " * " + A(1);
-      case K::Rcp: return "ff_rcp(" + A(0) + ")";
-      case K::Div: return "ff_div(" + A(0) + ", " + A(1) + ")";
-      case K::Exp2: return "ff_exp2(" + A(0) + ")";
-      case K::Log: return "ff_log(" + A(0) + ")";
-      case K::Sin: return "ff_sin(" + A(0) + ")";
-      case K::Cos: return "ff_cos(" + A(0) + ")";
-      case K::Tan: return "ff_tan(" + A(0) + ")";
-      case K::Tanh: return "ff_tanh(" + A(0) + ")";
-      case K::Sqrt: return "ff_sqrt(" + A(0) + ")";
-      case K::Abs: return "ff_abs(" + A(0) + ")";
-      case K::Min: return "ff_min(" + A(0) + ", " + A(1) + ")";
-      case K::Max: return "ff_max(" + A(0) + ", " + A(1) + ")";
-      case K::Pow: return "ff_pow(" + A(0) + ", " + A(1) + ")";
-      case K::Sigmoid2: return "ff_rcp(1.0f + ff_exp2(" + A(0) + "))";
-      case K::SelAbsLt: return "ff_sel_abs_lt(" + A(0) + ", " + A(1) + ", " + A(2) + ", " + flit(n.value) + ")";
-      default: throw Error(FF_ERR_COMPILE, "internal: unexpected node in expr()");
-    }
-  }
+  std::string expr(const DNode& n, F A) { return node_expr(n, A); }
 
   std::string get(Operand o) { return get(o.node, o.neg); }
 
@@ -778,6 +790,19 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select) {
   std::vector<int> roots;
   for (int i = 0; i < s.dim; ++i) roots.push_back(g.lower(s.rhs[i]));
 
+  // A component f_d = u * w with u uniform (loop-invariant) and w varying is emitted as w and the
+  // integrator folds u into its per-dimension step constants: x + (h/2) f = x + (h u / 2) w, and the
+  // stage sum accumulates w. Saves one multiply per component and evaluation (Lorenz: sigma (y - x),
+  // 4 of 44 FMA-pipe ops per particle-step); the scale is computed once per tile.
+  std::vector<int> scale(s.dim, -1);
+  for (int i = 0; i < s.dim; ++i) {
+    const DNode& n = g.nodes[roots[i]];
+    if (n.k == K::Mul && !n.uniform && g.nodes[n.a[0]].uniform) {
+      scale[i] = n.a[0];
+      roots[i] = n.a[1];
+    }
+  }
+
   // reachable nodes in topological (creation) order
   std::vector<char> live(g.nodes.size(), 0);
   std::function<void(int)> mark = [&](int x) {
@@ -803,7 +828,11 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select) {
   for (size_t k = 0; k < s.param_names.size(); ++k)
     rhs << "//   a.p[" << k << "] = " << s.param_names[k]
         << ((int)k == sweep_param ? "  (swept: the per-particle value sw is used instead)" : "") << "\n";
+  int n_scaled = 0;
+  for (int i = 0; i < s.dim; ++i) n_scaled += scale[i] >= 0;
   rhs << "// per evaluation (front-end count): " << n_arith << " arithmetic ops, " << n_mufu << " MUFU ops\n";
+  rhs << "// plain formulation (uniform factors multiplied in every evaluation): " << n_arith + n_scaled
+      << " arithmetic ops\n";
   rhs << "template <class V>\n__device__ __forceinline__ void ff_rhs(const V* __restrict__ x, V* __restrict__ dx, "
          "const FFStepArgs& a, const V& sw) {\n";
   rhs << "  (void)a; (void)sw;\n";
@@ -812,14 +841,18 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select) {
   for (int i = 0; i < s.dim; ++i) {
     const DNode& r = g.nodes[roots[i]];
     rhs << "  dx[" << i << "] = " << (r.uniform ? "ff_bcast<V>(" + out[i] + ")" : out[i]) << ";"
-        << (sign[i] < 0 ? "  // = -d" + s.var_names[i] + "/dt (FF_SIGN)" : "") << "\n";
+        << (sign[i] < 0 || scale[i] >= 0 ? "  // = d" + s.var_names[i] + "/dt / sc[" + std::to_string(i) + "]" : "")
+        << "\n";
   }
   rhs << "}\n";
-  rhs << "// dx[d] holds FF_SIGN[d] * f_d(x): a component computed negated saves FFMA2 negations; the\n"
-         "// integrator folds the sign into its (uniform) step constants.\n";
-  rhs << "__device__ constexpr float FF_SIGN[FF_DIM] = {";
-  for (int i = 0; i < s.dim; ++i) rhs << (i ? ", " : "") << (sign[i] < 0 ? "-1.0f" : "1.0f");
-  rhs << "};\n";
+  rhs << "// dx[d] holds f_d(x) / sc[d]: a component computed negated saves FFMA2 negations, a uniform\n"
+         "// factor saves a multiply; the integrator folds sc[d] into its (uniform) step constants.\n";
+  rhs << "__device__ __forceinline__ void ff_scales(const FFStepArgs& a, float* sc) {\n  (void)a;\n";
+  for (int i = 0; i < s.dim; ++i) {
+    std::string v = scale[i] >= 0 ? uexpr(g, scale[i]) : "1.0f";
+    rhs << "  sc[" << i << "] = " << (sign[i] < 0 ? "-" : "") << v << ";\n";
+  }
+  rhs << "}\n";
 
   const int dim = s.dim;
   int unroll = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);

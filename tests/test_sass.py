@@ -1,5 +1,7 @@
 """SASS checks of the generated kernels (CPU only: NVRTC + cuobjdump): the inner RK4 loop of the
-default Lorenz kernel issues exactly the expected FMA-pipe work, packed, without spills."""
+default Lorenz kernel issues exactly the expected FMA-pipe work, packed, without spills: 41 FP32
+lane-ops per particle-step (4 RHS evaluations x 5 -- sigma factored out of dx/dt into the step
+constants -- plus 3 dimensions x 7 for the stage inputs and the RK4 combination)."""
 import collections
 import re
 import subprocess
@@ -34,18 +36,18 @@ def lorenz_cubin(tmp_path_factory):
     return str(p)
 
 
-def test_packed_loop_is_44_lane_ops_per_particle_step_no_spills(lorenz_cubin):
+def test_packed_loop_is_41_lane_ops_per_particle_step_no_spills(lorenz_cubin):
     loops = [c for c in inner_loops(lorenz_cubin, "ff_step_p2_t128") if c["FFMA2"] >= 100]
     assert loops, "no packed RK4 loop found"
     main = min(loops, key=lambda c: sum(c.values()))   # innermost = the smallest loop body
     packed = main["FFMA2"] + main["FMUL2"] + main["FADD2"]
-    # unrolled x4, two particles per instruction: 4 steps x 2 particles x 44 lane-ops / 2 lanes
-    assert packed == 176
+    # unrolled x4, two particles per instruction: 4 steps x 2 particles x 41 lane-ops / 2 lanes
+    assert packed == 164
     assert main["LDL"] == 0 and main["STL"] == 0
     assert main["FFMA"] == 0 and main["FADD"] == 0 and main["FMUL"] == 0   # nothing left unpacked
 
 
-def test_scalar_loop_is_44_ops(lorenz_cubin):
+def test_scalar_loop_is_41_ops(lorenz_cubin):
     loops = [c for c in inner_loops(lorenz_cubin, "ff_step_p1_t256") if c["FFMA"] >= 100]
     main = min(loops, key=lambda c: sum(c.values()))
-    assert main["FFMA"] + main["FADD"] + main["FMUL"] == 176 and main["LDL"] == 0
+    assert main["FFMA"] + main["FADD"] + main["FMUL"] == 164 and main["LDL"] == 0
