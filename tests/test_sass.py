@@ -51,3 +51,14 @@ def test_scalar_loop_is_41_ops(lorenz_cubin):
     loops = [c for c in inner_loops(lorenz_cubin, "ff_step_p1_t256") if c["FFMA"] >= 100]
     main = min(loops, key=lambda c: sum(c.values()))
     assert main["FFMA"] + main["FADD"] + main["FMUL"] == 164 and main["LDL"] == 0
+
+
+def test_front_end_op_counts():
+    """Front-end counts per particle-step (4 RHS evaluations + 7 per dimension): the plain
+    formulation (the roofline's algorithmic work) and what the kernel executes after the uniform-
+    factor and gating-form rewrites (Lorenz: sigma folded into the step constants; HH: a(1-X) - bX
+    -> a - (a+b)X for the 12 gating equations)."""
+    import bench
+    assert bench.op_counts(systems.lorenz(), -1) == (45, 0, 41)
+    assert bench.op_counts(systems.hh_ring(3), -1) == (813, 84, 765)
+    assert bench.op_counts(systems.stn_gpe(), -1) == (62, 16, 54)
