@@ -15,6 +15,7 @@ typedef unsigned int ff_u32;
 #define FF_MAX_GROUPS_ 16
 #define FF_MAX_DIM_ 64
 #define FF_MAX_PEERS_ 8
+#define FF_MAX_SCALED_ 4  // components with a factored uniform scale (split_scales)
 // word offsets in the exchange sync block (each word on its own 128-byte line)
 #define FF_XS_ARRIVE 0
 #define FF_XS_GO 16
@@ -31,7 +32,9 @@ struct FFGroup {
   ff_i64 first_global;  // group-global index of the first local particle
   ff_i64 n_global;      // particles in the whole group (all shards)
   ff_u64 sweep_seed;
-  float h, h2, h6, pad0_;  // signed step direction*dt, h/2, h/6
+  float h, h2, h6;      // signed step direction*dt, h/2, h/6
+  float nh, nh2, nh6;   // -h, -h/2, -h/6 (host-negated: loaded straight into uniform registers)
+  float pad0_, pad1_;
   float sw_lo, sw_hi, sw_top, sw_val;  // sweep range, largest float below hi, uniform value
   int sweep_mode;       // -1: every particle uses sw_val; 0: Philox-uniform; 1: linspace
   int colour;           // image channel
@@ -69,6 +72,9 @@ struct FFStepArgs {
   int pad2_;
   float bound_lo[FF_MAX_DIM_], bound_hi[FF_MAX_DIM_];
   FFGroup g[FF_MAX_GROUPS_];
+  // step constants of the components with a factored uniform scale s (FF_SSLOT[d] in the generated
+  // code): {h s, h/2 s, h/6 s, -h s, -h/2 s, -h/6 s} per group and slot, computed by the host
+  float hs[FF_MAX_GROUPS_][FF_MAX_SCALED_][6];
   float p[FF_NP_ALLOC]; // parameter values (must stay the last member)
 };
 

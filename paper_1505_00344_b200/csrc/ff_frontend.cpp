@@ -194,6 +194,106 @@ struct Parser {
 
 }  // namespace
 
+// ---------------------------------------------------------------- uniform factors of components
+namespace {
+
+bool param_only(const NodeP& n, int sweep_param) {
+  if (n->op == Op::Var) return false;
+  if (n->op == Op::Param) return n->index != sweep_param;
+  for (const NodeP& a : n->args) if (!param_only(a, sweep_param)) return false;
+  return true;
+}
+
+NodeP mk(Op op, std::vector<NodeP> args, double v = 0.0) {
+  NodeP n = std::make_shared<Node>();
+  n->op = op;
+  n->value = v;
+  n->args = std::move(args);
+  return n;
+}
+
+// the factors of a product tree: a * b, a / c (c a factor 1/c when it is parameter-only), -a
+void factors(const NodeP& n, int sp, std::vector<NodeP>& uni, std::vector<NodeP>& var) {
+  if (n->op == Op::Mul) {
+    factors(n->args[0], sp, uni, var);
+    factors(n->args[1], sp, uni, var);
+  } else if (n->op == Op::Neg) {
+    uni.push_back(mk(Op::Num, {}, -1.0));
+    factors(n->args[0], sp, uni, var);
+  } else if (n->op == Op::Div && param_only(n->args[1], sp)) {
+    factors(n->args[0], sp, uni, var);
+    uni.push_back(mk(Op::Div, {mk(Op::Num, {}, 1.0), n->args[1]}));
+  } else if (param_only(n, sp)) {
+    uni.push_back(n);
+  } else {
+    var.push_back(n);
+  }
+}
+
+NodeP product(const std::vector<NodeP>& f) {
+  NodeP p = f[0];
+  for (size_t i = 1; i < f.size(); ++i) p = mk(Op::Mul, {p, f[i]});
+  return p;
+}
+
+}  // namespace
+
+std::vector<int> split_scales(const System& s, int sweep_param, std::vector<NodeP>* rest, std::vector<NodeP>* scale) {
+  std::vector<int> slot(s.dim, -1);
+  rest->assign(s.rhs.begin(), s.rhs.end());
+  scale->assign(s.dim, nullptr);
+  int used = 0;
+  for (int d = 0; d < s.dim && used < FF_MAX_SCALED; ++d) {
+    std::vector<NodeP> uni, var;
+    factors(s.rhs[d], sweep_param, uni, var);
+    if (uni.empty() || var.empty()) continue;  // nothing to factor out, or a constant derivative
+    // a lone -1 is left to the sign selection (free there)
+    if (uni.size() == 1 && uni[0]->op == Op::Num && uni[0]->value == -1.0) continue;
+    (*rest)[d] = product(var);
+    (*scale)[d] = product(uni);
+    slot[d] = used++;
+  }
+  return slot;
+}
+
+double eval_uniform(const NodeP& n, const std::vector<float>& p) {
+  auto A = [&](int i) { return eval_uniform(n->args[i], p); };
+  switch (n->op) {
+    case Op::Num: return n->value;
+    case Op::Param: return (double)p.at(n->index);
+    case Op::Neg: return -A(0);
+    case Op::Add: return A(0) + A(1);
+    case Op::Sub: return A(0) - A(1);
+    case Op::Mul: return A(0) * A(1);
+    case Op::Div: return A(0) / A(1);
+    case Op::Pow: return std::pow(A(0), A(1));
+    case Op::Var: throw Error(FF_ERR_STATE, "internal: state variable in a uniform factor");
+    case Op::Call: {
+      const std::string& f = n->name;
+      const double x = A(0);
+      if (f == "exp") return std::exp(x);
+      if (f == "log") return std::log(x);
+      if (f == "sin") return std::sin(x);
+      if (f == "cos") return std::cos(x);
+      if (f == "tan") return std::tan(x);
+      if (f == "tanh") return std::tanh(x);
+      if (f == "sqrt") return std::sqrt(x);
+      if (f == "abs") return std::fabs(x);
+      if (f == "sigmoid") return 1.0 / (1.0 + std::exp(-x));
+      const double y = A(1);
+      if (f == "pow") return std::pow(x, y);
+      if (f == "min") return std::fmin(x, y);
+      if (f == "max") return std::fmax(x, y);
+      if (f == "vtrap") {
+        const double u = x / y;
+        return std::fabs(u) < 0.1 ? y * (1.0 - u / 2.0 + u * u / 12.0 - u * u * u * u / 720.0) : x / std::expm1(u);
+      }
+      throw Error(FF_ERR_STATE, "internal: unknown function " + f);
+    }
+  }
+  return 0.0;
+}
+
 System parse_system(const ff_system* sys) {
   if (!sys) throw Error(FF_ERR_INVALID_ARG, "system is NULL");
   if (sys->dim < 1 || sys->dim > FF_MAX_DIM)
@@ -612,14 +712,6 @@ std::string node_expr(const DNode& n, F A) {
 }
 
 
-// inline expression of a uniform (loop-invariant) node, fully parenthesised
-std::string uexpr(const Dag& g, int id) {
-  const DNode& n = g.nodes[id];
-  if (n.k == K::Num) return flit(n.value);
-  if (n.k == K::Param) return "a.p[" + std::to_string(n.index) + "]";
-  return "(" + node_expr(n, [&](int j) { return uexpr(g, n.a[j]); }) + ")";
-}
-
 // ---------------------------------------------------------------- sign-aware instruction selection
 // FFMA2 / FADD2 / FMUL2 (the packed pair path) have no operand negation, so every "-v" of a
 // varying value costs an instruction, while negating a uniform (loop-invariant) value is free. For
@@ -660,6 +752,13 @@ struct SignSelect {
   }
 
   double cost(int id, int s) const { return c[s][id]; }
+  // An FFMA2 whose three operands are all per-particle registers runs at 87 lane-ops/clk/SM against
+  // 126 with an immediate or uniform operand (register-file read bandwidth; measured on B200,
+  // tools/ubench/pipes.cu): charge it ~0.45 extra issue, so a*b + u*c becomes fma(u, c, a*b)
+  // rather than fma(a, b, u*c) -- the same instruction count, faster.
+  double reg3(const Operand& x, const Operand& y, int z) const {
+    return (!g.nodes[x.node].uniform && !g.nodes[y.node].uniform && !g.nodes[z].uniform) ? 0.45 : 0.0;
+  }
   // a varying product whose every use is an addition / subtraction: each user absorbs it into an
   // FFMA (duplicating the multiply costs nothing), so it is never materialised on its own
   bool fusable(int id) const {
@@ -698,8 +797,14 @@ struct SignSelect {
         consider(1 + c[s][a] + c[sb ^ 1][b], {Choice::SUB, {{a, s}, {b, sb ^ 1}, {}}});
         consider(1 + c[sb][b] + c[s ^ 1][a], {Choice::SUB, {{b, sb}, {a, s ^ 1}, {}}});
         Operand x, y;
-        if (fusable(a)) { double v = 1 + prod(a, s, x, y) + c[sb][b]; consider(v, {Choice::FMA, {x, y, {b, sb}}}); }
-        if (fusable(b)) { double v = 1 + prod(b, sb, x, y) + c[s][a]; consider(v, {Choice::FMA, {x, y, {a, s}}}); }
+        if (fusable(a)) {
+          double v = 1 + prod(a, s, x, y) + c[sb][b] + reg3(x, y, b);
+          consider(v, {Choice::FMA, {x, y, {b, sb}}});
+        }
+        if (fusable(b)) {
+          double v = 1 + prod(b, sb, x, y) + c[s][a] + reg3(x, y, a);
+          consider(v, {Choice::FMA, {x, y, {a, s}}});
+        }
         break;
       }
       case K::Mul: {
@@ -853,24 +958,13 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select) {
     }
     n_arith_plain = sp.n_arith;
   }
-  // pass 2: lower with the sharing plan
+  // pass 2: lower with the sharing plan; split components are lowered without their uniform factor
+  std::vector<NodeP> rest, scale_ast;
+  const std::vector<int> slot = split_scales(s, sweep_param, &rest, &scale_ast);
   Dag g(sweep_param);
   g.plan = &plan;
   std::vector<int> roots;
-  for (int i = 0; i < s.dim; ++i) roots.push_back(g.lower(s.rhs[i]));
-
-  // A component f_d = u * w with u uniform (loop-invariant) and w varying is emitted as w and the
-  // integrator folds u into its per-dimension step constants: x + (h/2) f = x + (h u / 2) w, and the
-  // stage sum accumulates w. Saves one multiply per component and evaluation (Lorenz: sigma (y - x),
-  // 4 of 44 FMA-pipe ops per particle-step); the scale is computed once per tile.
-  std::vector<int> scale(s.dim, -1);
-  for (int i = 0; i < s.dim; ++i) {
-    const DNode& n = g.nodes[roots[i]];
-    if (n.k == K::Mul && !n.uniform && g.nodes[n.a[0]].uniform) {
-      scale[i] = n.a[0];
-      roots[i] = n.a[1];
-    }
-  }
+  for (int i = 0; i < s.dim; ++i) roots.push_back(g.lower(rest[i]));
 
   // reachable nodes in topological (creation) order
   std::vector<char> live(g.nodes.size(), 0);
@@ -908,19 +1002,20 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select) {
   for (int i = 0; i < s.dim; ++i) {
     const DNode& r = g.nodes[roots[i]];
     rhs << "  dx[" << i << "] = " << (r.uniform ? "ff_bcast<V>(" + out[i] + ")" : out[i]) << ";"
-        << (sign[i] < 0 || scale[i] >= 0 ? "  // = d" + s.var_names[i] + "/dt / sc[" + std::to_string(i) + "]" : "")
+        << (sign[i] < 0 || slot[i] >= 0 ? "  // = d" + s.var_names[i] + "/dt" + (sign[i] < 0 ? " * (-1)" : "") +
+                                              (slot[i] >= 0 ? " / scale" : "") : "")
         << "\n";
   }
   rhs << "}\n";
-  rhs << "// dx[d] holds f_d(x) / sc[d]: a component computed negated saves FFMA2 negations, a uniform\n"
-         "// factor saves a multiply; the integrator folds sc[d] into its (uniform) step constants.\n";
-  rhs << "__device__ __forceinline__ void ff_scales(const FFStepArgs& a, float* sc) {\n  (void)a;\n";
-  for (int i = 0; i < s.dim; ++i) {
-    std::string v = scale[i] >= 0 ? uexpr(g, scale[i]) : "1.0f";
-    rhs << "  sc[" << i << "] = " << (sign[i] < 0 ? "-" : "") << v << ";\n";
-  }
-  rhs << "}\n";
-
+  rhs << "// dx[d] holds FF_SIGN[d] * f_d(x) / scale_d: a component computed negated saves FFMA2\n"
+         "// negations, a uniform factor scale_d (slot FF_SSLOT[d] >= 0) saves a multiply; the integrator\n"
+         "// uses step constants with both folded in (host-computed per launch and group: FFStepArgs hs).\n";
+  rhs << "__device__ constexpr float FF_SIGN[FF_DIM] = {";
+  for (int i = 0; i < s.dim; ++i) rhs << (i ? ", " : "") << (sign[i] < 0 ? "-1.0f" : "1.0f");
+  rhs << "};\n";
+  rhs << "__device__ constexpr int FF_SSLOT[FF_DIM] = {";
+  for (int i = 0; i < s.dim; ++i) rhs << (i ? ", " : "") << slot[i];
+  rhs << "};\n";
   const int dim = s.dim;
   int unroll = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
   int minb_p1 = dim <= 4 ? 4 : (dim <= 8 ? 3 : (dim <= 16 ? 2 : 1));

@@ -9,6 +9,8 @@
 
 #include "fireflies.h"
 
+#define FF_MAX_SCALED 4  /* components with a factored uniform scale (ff_args.h FF_MAX_SCALED_) */
+
 namespace ff {
 
 // Error carried to the ABI boundary, where it becomes an ff_status + ff_last_error() message.
@@ -49,6 +51,17 @@ struct System {
 
 // Parse + validate an ff_system (throws Error).
 System parse_system(const ff_system* sys);
+
+// Uniform factors of the components ("instruction selection"): component d is written
+// f_d = scale_d * rest_d with scale_d a product of factors that depend on parameters only (not on
+// state variables, not on the swept parameter `sweep_param`). The kernel integrates rest_d with step
+// constants h * scale_d computed by the host per launch, so the RHS never multiplies by scale_d.
+// At most FF_MAX_SCALED components are split (the first ones); returns the slot of every component
+// (-1 = not split) and fills rest (every component) and scale (every split one, else null).
+std::vector<int> split_scales(const System& s, int sweep_param, std::vector<NodeP>* rest,
+                              std::vector<NodeP>* scale);
+// Value (double) of a parameter-only expression for the given parameter values.
+double eval_uniform(const NodeP& n, const std::vector<float>& params);
 
 // Emit the complete NVRTC source (generated prefix + device template) for the system with
 // parameter `sweep_param` (or -1) per-particle.

@@ -18,7 +18,8 @@
 #include "device/ff_args.h"
 #include "ff_internal.hpp"
 
-static_assert(sizeof(FFGroup) == 104, "FFGroup layout");
+static_assert(sizeof(FFGroup) == 120, "FFGroup layout");
+static_assert(FF_MAX_SCALED_ == FF_MAX_SCALED, "scaled-component table size");
 static_assert(offsetof(FFStepArgs, g) == 744, "FFStepArgs layout");
 static_assert(FF_MAX_PEERS_ == FF_MAX_PEERS, "peer table size");
 static_assert(FF_MAX_DIM_ == FF_MAX_DIM, "bounds table size");
@@ -199,6 +200,18 @@ struct ff_ctx {
     return m.step[id];
   }
 
+  // the uniform factors of the split components of a system variant, in slot order (cached)
+  std::map<int, std::vector<ff::NodeP>> scale_cache;
+  const std::vector<ff::NodeP>& scale_asts(int sweep) {
+    auto it = scale_cache.find(sweep);
+    if (it != scale_cache.end()) return it->second;
+    std::vector<ff::NodeP> rest, sc, out;
+    const std::vector<int> slot = ff::split_scales(sys, sweep, &rest, &sc);
+    for (int d = 0; d < sys.dim; ++d)
+      if (slot[d] >= 0) out.push_back(sc[d]);
+    return scale_cache.emplace(sweep, out).first->second;
+  }
+
   int find_param(const char* name) const {
     if (!name) throw ff::Error(FF_ERR_INVALID_ARG, "parameter name is NULL");
     for (size_t k = 0; k < sys.param_names.size(); ++k)
@@ -269,6 +282,9 @@ struct ff_ctx {
       a.bound_lo[d] = bound_lo[d];
       a.bound_hi[d] = bound_hi[d];
     }
+    // uniform factors of the split components (ff::split_scales), at the current parameter values
+    std::vector<float> scales;
+    for (const ff::NodeP& n : scale_asts(sweep_param)) scales.push_back((float)ff::eval_uniform(n, params));
     for (size_t gi = 0; gi < groups.size(); ++gi) {
       const GroupRec& G = groups[gi];
       FFGroup& g = a.g[gi];
@@ -284,6 +300,19 @@ struct ff_ctx {
       g.h = h;
       g.h2 = h * 0.5f;
       g.h6 = h / 6.0f;
+      g.nh = -g.h;
+      g.nh2 = -g.h2;
+      g.nh6 = -g.h6;
+      for (size_t k = 0; k < scales.size(); ++k) {
+        const float sc = scales[k];
+        float* q = a.hs[gi][k];
+        q[0] = g.h * sc;
+        q[1] = g.h2 * sc;
+        q[2] = g.h6 * sc;
+        q[3] = -q[0];
+        q[4] = -q[1];
+        q[5] = -q[2];
+      }
       g.colour = G.colour;
       g.sweep_mode = (sweep_param >= 0) ? G.sweep_mode : -1;
       g.sweep_seed = G.sw_seed;

@@ -178,6 +178,38 @@ __global__ void k_red(unsigned* img, int nbins, int reps, int aggregate) {
   }
 }
 
+
+// Packed FP32 with per-accumulator operands (no shared registers): does operand-register read
+// bandwidth limit FFMA2 / FADD2 / FMUL2 the way it limits FFMA(3reg)?
+#define PACKED_KERNEL(NAME, INIT, BODY)                                                             \
+  __global__ void NAME(const float* __restrict__ in, float* out, long long* cyc) {                  \
+    float2 a[NACC], b[NACC], c[NACC];                                                             \
+    _Pragma("unroll") for (int i = 0; i < NACC; ++i) {                                             \
+      a[i] = make_float2(in[2 + i] + threadIdx.x, in[2 + i] - threadIdx.x);                        \
+      b[i] = make_float2(in[0] * (1.f + i * 1e-7f), in[0] * (1.f - i * 1e-7f));                    \
+      c[i] = make_float2(in[1] * (1.f + i * 1e-7f), in[1] * (1.f - i * 1e-7f));                    \
+      INIT;                                                                                        \
+    }                                                                                              \
+    __syncthreads();                                                                               \
+    long long t0 = clock64();                                                                      \
+    _Pragma("unroll 4") for (int it = 0; it < ITERS; ++it) {                                       \
+      _Pragma("unroll") for (int i = 0; i < NACC; ++i) BODY;                                       \
+    }                                                                                              \
+    __syncthreads();                                                                               \
+    long long t1 = clock64();                                                                      \
+    float s = 0.f;                                                                                 \
+    _Pragma("unroll") for (int i = 0; i < NACC; ++i) s += a[i].x + a[i].y;                         \
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;                                                \
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;                                               \
+  }
+PACKED_KERNEL(k_ffma2_3reg, (void)0, a[i] = __ffma2_rn(a[i], b[i], c[i]))
+PACKED_KERNEL(k_ffma2_2reg, (void)0, a[i] = __ffma2_rn(a[i], b[i], make_float2(0.5f, 0.5f)))
+PACKED_KERNEL(k_fadd2_2reg, c[i] = make_float2(-c[i].x * 1e-9f, c[i].y * 1e-9f), a[i] = __fadd2_rn(a[i], c[i]))
+// scalar broadcast operand from a per-thread register (R.F32) vs a kernel parameter (UR / constant)
+PACKED_KERNEL(k_ffma2_rscalar, b[i] = make_float2(1.0f + threadIdx.x * 1e-9f + i * 1e-8f, 0.f),
+              a[i] = __ffma2_rn(make_float2(b[i].x, b[i].x), a[i], c[i]))
+PACKED_KERNEL(k_fmul2_2reg, b[i] = make_float2(1.0000001f, 0.9999999f), a[i] = __fmul2_rn(a[i], b[i]))
+
 typedef void (*kfn)(const float*, float*, long long*);
 
 static double run(const char* name, kfn k, double ops_per_thread_iter, int iters, int nsm, int threads,
@@ -224,6 +256,11 @@ int main() {
     run("FFMA(3reg)", k_ffma_reg3, NACC, ITERS, nsm, 1024, din, dout, dcyc);
     run("FFMA2", k_ffma2, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
     run("FADD", k_fadd, NACC, ITERS, nsm, 1024, din, dout, dcyc);
+    run("FFMA2(3reg)", k_ffma2_3reg, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
+    run("FFMA2(2reg+k)", k_ffma2_2reg, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
+    run("FADD2(2reg)", k_fadd2_2reg, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
+    run("FMUL2(2reg)", k_fmul2_2reg, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
+    run("FFMA2(Rscal)", k_ffma2_rscalar, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
     run("MUFU.EX2", k_ex2, NACC, ITERS / 4, nsm, 1024, din, dout, dcyc);
     run("MUFU.RCP", k_rcp, NACC, ITERS / 4, nsm, 1024, din, dout, dcyc);
     run("FFMA4+EX2", k_mix, 5 * NACC, ITERS / 4, nsm, 1024, din, dout, dcyc);
