@@ -16,6 +16,7 @@ typedef unsigned int ff_u32;
 #define FF_MAX_DIM_ 64
 #define FF_MAX_PEERS_ 8
 #define FF_MAX_SCALED_ 4  // components with a factored uniform scale (split_scales)
+#define FF_MAX_DERIVED_ 192  // host-evaluated loop-invariant values of the RHS (ff::UProgram)
 // word offsets in the exchange sync block (each word on its own 128-byte line)
 #define FF_XS_ARRIVE 0
 #define FF_XS_GO 16
@@ -75,6 +76,9 @@ struct FFStepArgs {
   // step constants of the components with a factored uniform scale s (FF_SSLOT[d] in the generated
   // code): {h s, h/2 s, h/6 s, -h s, -h/2 s, -h/6 s} per group and slot, computed by the host
   float hs[FF_MAX_GROUPS_][FF_MAX_SCALED_][6];
+  // loop-invariant values of the generated RHS (products / reciprocals / exponentials of parameters,
+  // negated parameters), evaluated by the host at every launch: uniform-register operands
+  float q[FF_MAX_DERIVED_];
   float p[FF_NP_ALLOC]; // parameter values (must stay the last member)
 };
 

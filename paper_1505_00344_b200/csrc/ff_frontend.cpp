@@ -832,6 +832,20 @@ struct SignSelect {
     return bc;
   }
 
+  // host-evaluated loop-invariant values: (node, negate) -> q slot
+  std::map<std::pair<int, int>, int> qslot;
+  std::vector<std::pair<int, int>> qlist;
+  std::string qref(int id, int s) {
+    auto key = std::make_pair(id, s);
+    auto it = qslot.find(key);
+    if (it != qslot.end()) return "a.q[" + std::to_string(it->second) + "]";
+    if ((int)qlist.size() >= FF_MAX_DERIVED) return "";
+    const int k = (int)qlist.size();
+    qlist.push_back(key);
+    qslot[key] = k;
+    return "a.q[" + std::to_string(k) + "]";
+  }
+
   std::string ureference(int id) {
     if (!uref[id].empty()) return uref[id];
     const DNode& n = g.nodes[id];
@@ -857,6 +871,9 @@ struct SignSelect {
     const DNode& n = g.nodes[id];
     if (n.uniform) {
       if (n.k == K::Num) return flit(s ? -n.value : n.value);
+      if (n.k == K::Param && !s) return "a.p[" + std::to_string(n.index) + "]";
+      const std::string q = qref(id, s);   // computed by the host (UProgram), read from the constant bank
+      if (!q.empty()) return q;
       return s ? "(-" + ureference(id) + ")" : ureference(id);
     }
     if (n.k == K::Neg) return get(n.a[0], s ^ 1);
@@ -909,7 +926,45 @@ struct SignSelect {
 
 }  // namespace
 
-std::string emit_source(const System& s, int sweep_param, int kernel_select) {
+std::vector<float> eval_program(const UProgram& prog, const std::vector<float>& p) {
+  std::vector<double> v(prog.ops.size());
+  for (size_t i = 0; i < prog.ops.size(); ++i) {
+    const UProgram::Op& o = prog.ops[i];
+    auto A = [&](int j) { return v[o.a[j]]; };
+    double r = 0.0;
+    switch ((K)o.kind) {
+      case K::Num: r = o.value; break;
+      case K::Param: r = (double)p.at(o.index); break;
+      case K::Neg: r = -A(0); break;
+      case K::Add: r = A(0) + A(1); break;
+      case K::Sub: r = A(0) - A(1); break;
+      case K::Mul: r = A(0) * A(1); break;
+      case K::Rcp: r = 1.0 / A(0); break;
+      case K::Div: r = A(0) / A(1); break;
+      case K::Exp2: r = std::exp2(A(0)); break;
+      case K::Log: r = std::log(A(0)); break;
+      case K::Sin: r = std::sin(A(0)); break;
+      case K::Cos: r = std::cos(A(0)); break;
+      case K::Tan: r = std::tan(A(0)); break;
+      case K::Tanh: r = std::tanh(A(0)); break;
+      case K::Sqrt: r = std::sqrt(A(0)); break;
+      case K::Abs: r = std::fabs(A(0)); break;
+      case K::Min: r = std::fmin(A(0), A(1)); break;
+      case K::Max: r = std::fmax(A(0), A(1)); break;
+      case K::Pow: r = std::pow(A(0), A(1)); break;
+      case K::Sigmoid2: r = 1.0 / (1.0 + std::exp2(A(0))); break;
+      case K::SelAbsLt: r = std::fabs(A(0)) < o.value ? A(1) : A(2); break;
+      case K::Var:
+      case K::Sweep: throw Error(FF_ERR_STATE, "internal: per-particle value in a uniform program");
+    }
+    v[i] = r;
+  }
+  std::vector<float> q;
+  for (const auto& e : prog.q) q.push_back((float)(e.second ? -v[e.first] : v[e.first]));
+  return q;
+}
+
+std::string emit_source(const System& s, int sweep_param, int kernel_select, UProgram* prog) {
   if (sweep_param < -1 || sweep_param >= (int)s.param_names.size())
     throw Error(FF_ERR_INVALID_ARG, "sweep parameter index out of range");
   // pass 1: lower once to find exponentials sharing an affine argument c w + d
@@ -984,6 +1039,21 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select) {
     out[i] = sel.get(r, sign[i] < 0 ? 1 : 0);
   }
   const int n_arith = sel.n_arith, n_mufu = sel.n_mufu;
+  if (prog) {  // the q values as a host program: every uniform node they reach, in creation order
+    prog->ops.clear();
+    prog->q.clear();
+    std::map<int, int> at;
+    std::function<int(int)> put = [&](int id) -> int {
+      auto it = at.find(id);
+      if (it != at.end()) return it->second;
+      const DNode& n = g.nodes[id];
+      UProgram::Op o{(int)n.k, n.value, n.index, {0, 0, 0}};
+      for (size_t j = 0; j < n.a.size() && j < 3; ++j) o.a[j] = put(n.a[j]);
+      prog->ops.push_back(o);
+      return at[id] = (int)prog->ops.size() - 1;
+    };
+    for (const auto& e : sel.qlist) prog->q.push_back({put(e.first), e.second});
+  }
   std::ostringstream rhs;
   rhs << "// Generated right-hand side (" << s.dim << " state variables, " << s.param_names.size()
       << " parameters, swept parameter index " << sweep_param << ").\n";

@@ -10,6 +10,7 @@
 #include "fireflies.h"
 
 #define FF_MAX_SCALED 4  /* components with a factored uniform scale (ff_args.h FF_MAX_SCALED_) */
+#define FF_MAX_DERIVED 192  /* host-evaluated loop-invariant values (ff_args.h FF_MAX_DERIVED_) */
 
 namespace ff {
 
@@ -63,11 +64,22 @@ std::vector<int> split_scales(const System& s, int sweep_param, std::vector<Node
 // Value (double) of a parameter-only expression for the given parameter values.
 double eval_uniform(const NodeP& n, const std::vector<float>& params);
 
+// Loop-invariant values of the generated RHS (products / reciprocals / exponentials of parameters,
+// negated parameters), evaluated by the host at every launch and passed in the parameter block
+// (FFStepArgs::q), so the kernel reads them as uniform-register operands instead of computing them
+// per thread (a per-thread register scalar operand costs FFMA2 throughput).
+struct UProgram {
+  struct Op { int kind; double value; int index; int a[3]; };
+  std::vector<Op> ops;                  // topological order; kind = front-end node kind
+  std::vector<std::pair<int, int>> q;   // per q slot: (op index, negate)
+};
+std::vector<float> eval_program(const UProgram& prog, const std::vector<float>& params);
+
 // Emit the complete NVRTC source (generated prefix + device template) for the system with
 // parameter `sweep_param` (or -1) per-particle.
 // kernel_select: which kernels the program defines (FF_KSEL in ff_device.cuh: 0-11 one step variant,
-// 100 = init + render, 255 = all).
-std::string emit_source(const System& s, int sweep_param, int kernel_select = 255);
+// 100 = init + render, 255 = all). prog (optional) receives the host program of the q values.
+std::string emit_source(const System& s, int sweep_param, int kernel_select = 255, UProgram* prog = nullptr);
 
 // NVRTC: source -> sm_100a CUBIN (throws Error(FF_ERR_COMPILE) with the log).
 std::vector<char> compile_cubin(const std::string& source, const std::string& name);

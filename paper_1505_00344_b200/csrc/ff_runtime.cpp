@@ -20,6 +20,7 @@
 
 static_assert(sizeof(FFGroup) == 120, "FFGroup layout");
 static_assert(FF_MAX_SCALED_ == FF_MAX_SCALED, "scaled-component table size");
+static_assert(FF_MAX_DERIVED_ == FF_MAX_DERIVED, "derived-value table size");
 static_assert(offsetof(FFStepArgs, g) == 744, "FFStepArgs layout");
 static_assert(FF_MAX_PEERS_ == FF_MAX_PEERS, "peer table size");
 static_assert(FF_MAX_DIM_ == FF_MAX_DIM, "bounds table size");
@@ -212,6 +213,16 @@ struct ff_ctx {
     return scale_cache.emplace(sweep, out).first->second;
   }
 
+  // host program of the RHS's loop-invariant values of a system variant (cached)
+  std::map<int, ff::UProgram> prog_cache;
+  const ff::UProgram& uprogram(int sweep) {
+    auto it = prog_cache.find(sweep);
+    if (it != prog_cache.end()) return it->second;
+    ff::UProgram prog;
+    ff::emit_source(sys, sweep, 100, &prog);
+    return prog_cache.emplace(sweep, prog).first->second;
+  }
+
   int find_param(const char* name) const {
     if (!name) throw ff::Error(FF_ERR_INVALID_ARG, "parameter name is NULL");
     for (size_t k = 0; k < sys.param_names.size(); ++k)
@@ -322,6 +333,10 @@ struct ff_ctx {
       g.sw_val = sweep_param >= 0 ? params[sweep_param] : 0.0f;
     }
     for (size_t k = 0; k < params.size(); ++k) a.p[k] = params[k];
+    {
+      const std::vector<float> q = ff::eval_program(uprogram(sweep_param), params);
+      for (size_t k = 0; k < q.size(); ++k) a.q[k] = q[k];
+    }
     const int64_t tile = (int64_t)p * t;
     const int64_t ntiles = next_slot / tile;
     if (ntiles == 0) {
