@@ -305,21 +305,42 @@ def run_ours(args, w, rank, world, device):
                 t_wall=t_wall)
 
 
+EXP2P_OPS = 8   # FMA-pipe ops of one exponential computed on the FMA pipe (ff_exp2p in ff_device.cuh)
+
+
 def op_counts(sysdef, sweep_idx):
-    """(algorithmic FMA-pipe lane-ops, MUFU ops, generated FMA-pipe lane-ops) per particle-step.
+    """Work per particle-step: (algorithmic FMA-pipe lane-ops, algorithmic MUFU ops, exponentials,
+    generated FMA-pipe lane-ops, generated MUFU ops).
 
     Algorithmic = the plain formulation of the system (as written: no gating-form rewrite, every
-    uniform factor of dx/dt multiplied in each of the 4 evaluations) + the RK4 combination (7 per
-    dimension): a fixed per-system constant
-    (SURVEY.md 8(d)), so work the front end saves raises the fraction instead of shrinking the
-    denominator. Generated = the front end's count of what the kernel actually executes."""
+    uniform factor of dx/dt multiplied in each of the 4 evaluations, every exponential on MUFU) + the
+    RK4 combination (7 per dimension): a fixed per-system constant, so work the front
+    end saves raises the fraction instead of shrinking the denominator. Generated = the front end's
+    count of what the kernel actually executes."""
     import re
     import paper_1505_00344_b200 as FF
     src = FF.ff_emit_source(sysdef, sweep_idx)
     m = re.search(r"per evaluation \(front-end count\): (\d+) arithmetic ops, (\d+) MUFU ops", src)
     p = re.search(r"plain formulation \(no gating rewrite, uniform factors multiplied in every evaluation\): "
-                  r"(\d+) arithmetic ops", src)
-    return (4 * int(p.group(1)) + 7 * sysdef.dim, 4 * int(m.group(2)), 4 * int(m.group(1)) + 7 * sysdef.dim)
+                  r"(\d+) arithmetic ops, (\d+) MUFU ops, (\d+) exponentials", src)
+    return (4 * int(p.group(1)) + 7 * sysdef.dim, 4 * int(p.group(2)), 4 * int(p.group(3)),
+            4 * int(m.group(1)) + 7 * sysdef.dim, 4 * int(m.group(2)))
+
+
+def balanced_work(fma_ops, mufu_ops, n_exp):
+    """FP32-pipe-equivalent work per particle-step of the pipe-balanced roofline: the FMA and MUFU
+    pipes run concurrently (128 and 16 results / clk / SM) and any exponential can move from MUFU to
+    the FMA pipe at EXP2P_OPS ops, so the least time per particle-step on one SM is
+    T = min_k max((mufu - k) / 16, (fma + EXP2P_OPS k) / 128) cycles; work = 128 T lane-ops (= fma
+    for an FMA-bound system). Returns (work, k, binding pipes)."""
+    best = (max(mufu_ops / XU_LANES, fma_ops / FMA_LANES), 0)
+    for k in range(1, n_exp + 1):
+        t = max((mufu_ops - k) / XU_LANES, (fma_ops + EXP2P_OPS * k) / FMA_LANES)
+        if t < best[0] - 1e-12:
+            best = (t, k)
+    t, k = best
+    pipes = "fma" if fma_ops / FMA_LANES >= mufu_ops / XU_LANES and k == 0 else ("xu" if k == 0 else "fma+xu")
+    return FMA_LANES * t, k, pipes
 
 
 def cpu_oracle_sample(w, n_sample, S):
@@ -429,17 +450,18 @@ def main():
     kern_s = r["kern_ms"] * 1e-3
     per_launch = r["n_local"] * r["S"]
     # Algorithmic work per particle-step: the plain formulation's FMA-pipe ops (4 RHS evaluations) plus
-    # the RK4 combination (7 per dimension); Lorenz: 4 x 6 + 3 x 7 = 45 (the kernel executes 41).
+    # the RK4 combination (7 per dimension) and its MUFU ops; Lorenz: 4 x 6 + 3 x 7 = 45 (the kernel
+    # executes 41). The ALU roofline is pipe-balanced (balanced_work): FMA-bound systems report against
+    # the FP32 peak as before; a MUFU-bound one against the least time both pipes together need.
     sysdef = make_system(w["system"])
-    fma_ops, mufu_ops, gen_ops = op_counts(sysdef, r["sweep_idx"])
+    fma_ops, mufu_ops, n_exp, gen_ops, gen_mufu = op_counts(sysdef, r["sweep_idx"])
+    work, k_bal, alu_pipes = balanced_work(fma_ops, mufu_ops, n_exp)
     dim = sysdef.dim
     cands = {
-        "fma": (per_launch * fma_ops / kern_s, N_SM * FMA_LANES * f_max,
-                "Tops/s (FP32 FMA-pipe lane-ops, a*b+c = 1 op)",
-                f"148 SM x 128 FP32 lanes x {f_max / 1e6:.0f} MHz (MEASURED_PEAKS sm_max_mhz; FFMA2 measured at "
-                "128 lanes/clk, profiles/r01_ubench_pipes.txt)", fma_ops),
-        "xu": (per_launch * mufu_ops / kern_s, N_SM * XU_LANES * f_max, "Tops/s (MUFU ex2/rcp results)",
-               f"148 SM x 16 MUFU/clk x {f_max / 1e6:.0f} MHz (profiles/r01_ubench_pipes.txt)", mufu_ops),
+        "alu": (per_launch * work / kern_s, N_SM * FMA_LANES * f_max,
+                "Tops/s (FP32-pipe-equivalent lane-ops of the pipe-balanced work, a*b+c = 1 op)",
+                f"148 SM x 128 FP32 lanes x {f_max / 1e6:.0f} MHz (MEASURED_PEAKS sm_max_mhz; FFMA2 / FADD2 / "
+                "FMUL2 measured at 126 lane-ops/clk/SM, MUFU 16/clk/SM: profiles/r01_ubench_pipes.txt)", work),
         "hbm": (r["n_local"] * 8 * dim / kern_s, peaks.get("hbm_gbs", 6549.1) * 1e9, "GB/s",
                 "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)", 8 * dim / r["S"]),
     }
@@ -447,9 +469,13 @@ def main():
     pipe = max(fracs, key=fracs.get)
     ach, peak, unit, src, per_unit = cands[pipe]
     scale = 1e9 if pipe == "hbm" else 1e12
-    roof = {"bound": "hbm" if pipe == "hbm" else "alu", "pipe": pipe, "unit": unit, "achieved": ach / scale,
+    roof = {"bound": "hbm" if pipe == "hbm" else "alu", "pipe": pipe if pipe == "hbm" else alu_pipes,
+            "unit": unit, "achieved": ach / scale,
             "peak": peak / scale, "frac": ach / peak, "peak_source": src,
-            "alg_per_particle_step": per_unit, "generated_fma_ops_per_particle_step": gen_ops,
+            "alg_per_particle_step": per_unit,
+            "work": {"fma_ops": fma_ops, "mufu_ops": mufu_ops, "exponentials": n_exp,
+                     "balanced_exponentials_on_fma": k_bal,
+                     "generated_fma_ops": gen_ops, "generated_mufu_ops": gen_mufu},
             "fracs_all_pipes": fracs,
             "kernel": "ff_step (integrate S steps + project + count, one launch)"}
     roof["traffic"] = None
@@ -464,7 +490,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": r["t_total_ms"] / args.steps, "higher_is_better": True,
             "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Philox ICs from the paper's IC boxes)", "config": config,
-            "pct_fp32_peak": 100 * fracs["fma"],
+            "pct_fp32_peak": 100 * fracs["alu"],
             "roofline": roof, "clocks": clocks, "gpu_launches": r["launches"], "e2e": r["e2e"],
             "kernel_ms_mean": r["kern_ms"], "frame_ms_p10_p50_p90": [float(np.percentile(r["frame_ms"], q))
                                                                      for q in (10, 50, 90)],

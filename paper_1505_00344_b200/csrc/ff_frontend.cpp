@@ -731,8 +731,10 @@ struct SignSelect {
   std::ostringstream body;
   int n_arith = 0, n_mufu = 0, tmp = 0;
 
-  SignSelect(const Dag& dag, const std::vector<char>& lv, const std::vector<int>& roots)
-      : g(dag), live(lv), uses(dag.nodes.size(), 0), uref(dag.nodes.size()) {
+  std::set<int> emul;  // exponentials computed on the FMA pipe (ff_exp2p) instead of MUFU.EX2
+  static constexpr int kExp2pOps = 8;
+  SignSelect(const Dag& dag, const std::vector<char>& lv, const std::vector<int>& roots, std::set<int> em = {})
+      : g(dag), live(lv), uses(dag.nodes.size(), 0), uref(dag.nodes.size()), emul(std::move(em)) {
     c[0].assign(g.nodes.size(), 0.0);
     c[1].assign(g.nodes.size(), 0.0);
     addsub_uses.assign(g.nodes.size(), 0);
@@ -897,6 +899,17 @@ struct SignSelect {
         case Choice::DIV: e = "ff_div(" + get(ch.op[0]) + ", " + get(ch.op[1]) + ")"; ++n_arith; ++n_mufu; break;
         case Choice::OTHER:
           if (n.k == K::Rcp) { e = "ff_rcp(" + get(ch.op[0]) + ")"; ++n_mufu; break; }
+          if (emul.count(id) && n.k == K::Exp2) {  // on the FMA pipe (pipe balancing)
+            e = "ff_exp2p(" + get(n.a[0], 0) + ")";
+            n_arith += kExp2pOps;
+            break;
+          }
+          if (emul.count(id) && n.k == K::Sigmoid2) {
+            e = "ff_rcp(1.0f + ff_exp2p(" + get(n.a[0], 0) + "))";
+            n_arith += kExp2pOps + 1;
+            ++n_mufu;
+            break;
+          }
           e = expr(n, [&](int j) { return get(n.a[j], 0); });
           count(n);
           break;
@@ -992,7 +1005,7 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   }
   // the plain formulation's op count (no gating rewrite, no factored scales): the fixed algorithmic
   // work per evaluation that bench.py's roofline counts
-  int n_arith_plain = 0;
+  int n_arith_plain = 0, n_mufu_plain = 0, n_exp_plain = 0;
   {
     Dag gp(sweep_param);
     gp.plan = &plan;
@@ -1012,6 +1025,10 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
       sp.get(r, (!gp.nodes[r].uniform && sp.cost(r, 1) < sp.cost(r, 0)) ? 1 : 0);
     }
     n_arith_plain = sp.n_arith;
+    n_mufu_plain = sp.n_mufu;
+    for (size_t id = 0; id < gp.nodes.size(); ++id)
+      if (lv[id] && !gp.nodes[id].uniform && (gp.nodes[id].k == K::Exp2 || gp.nodes[id].k == K::Sigmoid2))
+        ++n_exp_plain;
   }
   // pass 2: lower with the sharing plan; split components are lowered without their uniform factor
   std::vector<NodeP> rest, scale_ast;
@@ -1030,7 +1047,31 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   };
   for (int r : roots) mark(r);
 
-  SignSelect sel(g, live, roots);
+  // Pipe balancing: a system bound by the MUFU pipe (16 results / clk / SM against 128 FP32 lanes)
+  // computes some of its exponentials with ff_exp2p on the FMA pipe instead (8 FMA-pipe ops each);
+  // k minimises max(MUFU work / 16, FMA work / 128) per evaluation (RK4 combination included).
+  std::set<int> emul;
+  {
+    SignSelect probe(g, live, roots);
+    for (int i = 0; i < s.dim; ++i) {
+      const int r = roots[i];
+      probe.get(r, (!g.nodes[r].uniform && probe.cost(r, 1) < probe.cost(r, 0)) ? 1 : 0);
+    }
+    std::vector<int> cand;
+    for (size_t id = 0; id < g.nodes.size(); ++id)
+      if (live[id] && !g.nodes[id].uniform && (g.nodes[id].k == K::Exp2 || g.nodes[id].k == K::Sigmoid2))
+        cand.push_back((int)id);
+    const double a = probe.n_arith + 7.0 * s.dim / 4.0, m = probe.n_mufu;
+    int best_k = 0;
+    double best_t = std::max(m / 16.0, a / 128.0);
+    for (int k = 1; k <= (int)cand.size(); ++k) {
+      const double t = std::max((m - k) / 16.0, (a + SignSelect::kExp2pOps * k) / 128.0);
+      if (t < best_t - 1e-9) { best_t = t; best_k = k; }
+    }
+    if (const char* e = std::getenv("FF_TUNE_EXP2P")) best_k = std::min((int)cand.size(), std::max(0, std::atoi(e)));
+    for (int k = 0; k < best_k; ++k) emul.insert(cand[k]);
+  }
+  SignSelect sel(g, live, roots, emul);
   std::vector<int> sign(s.dim, 1);
   std::vector<std::string> out(s.dim);
   for (int i = 0; i < s.dim; ++i) {
@@ -1062,8 +1103,9 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
     rhs << "//   a.p[" << k << "] = " << s.param_names[k]
         << ((int)k == sweep_param ? "  (swept: the per-particle value sw is used instead)" : "") << "\n";
   rhs << "// per evaluation (front-end count): " << n_arith << " arithmetic ops, " << n_mufu << " MUFU ops\n";
+  rhs << "// exponentials on the FMA pipe (pipe balancing): " << emul.size() << "\n";
   rhs << "// plain formulation (no gating rewrite, uniform factors multiplied in every evaluation): "
-      << n_arith_plain << " arithmetic ops\n";
+      << n_arith_plain << " arithmetic ops, " << n_mufu_plain << " MUFU ops, " << n_exp_plain << " exponentials\n";
   rhs << "template <class V>\n__device__ __forceinline__ void ff_rhs(const V* __restrict__ x, V* __restrict__ dx, "
          "const FFStepArgs& a, const V& sw) {\n";
   rhs << "  (void)a; (void)sw;\n";

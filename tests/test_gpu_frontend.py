@@ -31,3 +31,43 @@ def test_all_builtin_functions(ppt, tpb):
     ctx.step(20, 0.01)
     want = O.rk4(O.FUNCS, O.ic_uniform(lo, hi, 31, 0, n), np.array([1.3, 0.7], np.float32), np.float32(0.01), 20)
     assert tier_a(ctx.read_state(g), want, dim_scales(lo, hi)) <= 1e-5
+
+
+@pytest.mark.parametrize("ppt,tpb", [(1, 256), (2, 128), (4, 128)])
+def test_exponentials_on_the_fma_pipe(monkeypatch, ppt, tpb):
+    """Pipe balancing: with FF_TUNE_EXP2P forcing every exponential (exp, sigmoid) of the FUNCS system
+    onto the FMA pipe (ff_exp2p: range reduction + degree-5 polynomial), the result still meets Tier A
+    against the oracle (libm exp)."""
+    monkeypatch.setenv("FF_TUNE_EXP2P", "99")
+    n, lo, hi = 9000 + 5, [-2.0, -2.0, -1.5], [2.0, 2.0, 1.5]
+    src = FF.ff_emit_source(FUNCS)
+    assert "ff_exp2p(" in src and "exponentials on the FMA pipe (pipe balancing): 2" in src
+    ctx = FF.Context(FUNCS, [n])
+    ctx.set_launch(ppt, tpb)
+    g = ctx.init_group(lo, hi, n, 1, 0, seed=31)
+    ctx.step(20, 0.01)
+    want = O.rk4(O.FUNCS, O.ic_uniform(lo, hi, 31, 0, n), np.array([1.3, 0.7], np.float32), np.float32(0.01), 20)
+    assert tier_a(ctx.read_state(g), want, dim_scales(lo, hi)) <= 1e-5
+
+
+def test_exp2p_extreme_arguments():
+    """ff_exp2p clamps its argument to [-126, 126]: exp of very negative arguments gives ~0 and of
+    very positive ones a huge positive value (the RK4 sum may then overflow to +inf, as with MUFU) --
+    never NaN or garbage exponent bits; sigmoid saturates to 0 / 1."""
+    import os
+    os.environ["FF_TUNE_EXP2P"] = "99"
+    try:
+        sysd = SystemDef("ext", ["x", "y"], ["exp(x) * 1e-30", "sigmoid(y)"], [])
+        n = 512
+        ctx = FF.Context(sysd, [n])
+        g = ctx.init_group([-500.0, -500.0], [500.0, 500.0], n, 1, 0, seed=3)
+        x0 = ctx.read_state(g)
+        ctx.step(1, 1e-3)
+        got = ctx.read_state(g)
+    finally:
+        del os.environ["FF_TUNE_EXP2P"]
+    assert not np.any(np.isnan(got))
+    assert np.all(got[0][x0[0] < -100] == x0[0][x0[0] < -100])    # exp -> ~0: x unchanged
+    assert np.all(got[0][x0[0] > 90] > x0[0][x0[0] > 90])          # huge positive (or +inf)
+    s = (got[1] - x0[1]).astype(np.float64) / 1e-3
+    assert np.all(np.abs(s[x0[1] > 100] - 1) < 0.1) and np.all(np.abs(s[x0[1] < -100]) < 0.1)   # ulp(400) = 3e-5
