@@ -977,7 +977,7 @@ std::vector<float> eval_program(const UProgram& prog, const std::vector<float>& 
   return q;
 }
 
-std::string emit_source(const System& s, int sweep_param, int kernel_select, UProgram* prog) {
+std::string emit_source(const System& s, int sweep_param, int kernel_select, UProgram* prog, bool balance) {
   if (sweep_param < -1 || sweep_param >= (int)s.param_names.size())
     throw Error(FF_ERR_INVALID_ARG, "sweep parameter index out of range");
   // pass 1: lower once to find exponentials sharing an affine argument c w + d
@@ -1051,7 +1051,7 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   // computes some of its exponentials with ff_exp2p on the FMA pipe instead (8 FMA-pipe ops each);
   // k minimises max(MUFU work / 16, FMA work / 128) per evaluation (RK4 combination included).
   std::set<int> emul;
-  {
+  if (balance) {
     SignSelect probe(g, live, roots);
     for (int i = 0; i < s.dim; ++i) {
       const int r = roots[i];

@@ -79,7 +79,10 @@ std::vector<float> eval_program(const UProgram& prog, const std::vector<float>& 
 // parameter `sweep_param` (or -1) per-particle.
 // kernel_select: which kernels the program defines (FF_KSEL in ff_device.cuh: 0-11 one step variant,
 // 100 = init + render, 255 = all). prog (optional) receives the host program of the q values.
-std::string emit_source(const System& s, int sweep_param, int kernel_select = 255, UProgram* prog = nullptr);
+// balance: let a MUFU-bound system compute some exponentials on the FMA pipe (throughput variant;
+// launches too small to fill the GPU use balance = false: the polynomial lengthens the RK4 chain).
+std::string emit_source(const System& s, int sweep_param, int kernel_select = 255, UProgram* prog = nullptr,
+                        bool balance = true);
 
 // NVRTC: source -> sm_100a CUBIN (throws Error(FF_ERR_COMPILE) with the log).
 std::vector<char> compile_cubin(const std::string& source, const std::string& name);

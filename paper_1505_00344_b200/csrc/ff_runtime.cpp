@@ -47,9 +47,10 @@ struct Module {
   // +6 = the same with position-linear colour compiled in (ff_project_colour), +12 = with the fused
   // image exchange (ff_set_exchange)
   cudaKernel_t exchange = nullptr;  // (in base_lib)
-  cudaLibrary_t step_lib[12] = {};
-  cudaKernel_t step[12] = {};
-  int occ[12] = {};
+  // [balanced][id]: balanced = exponentials shared with the FMA pipe (emit_source balance)
+  cudaLibrary_t step_lib[2][12] = {};
+  cudaKernel_t step[2][12] = {};
+  int occ[2][12] = {};
 };
 
 constexpr int kNumStep = 6;
@@ -126,8 +127,9 @@ struct ff_ctx {
   ~ff_ctx() {
     for (auto& m : modules) {
       if (m.second.base_lib) cudaLibraryUnload(m.second.base_lib);
-      for (cudaLibrary_t l : m.second.step_lib)
-        if (l) cudaLibraryUnload(l);
+      for (auto& row : m.second.step_lib)
+        for (cudaLibrary_t l : row)
+          if (l) cudaLibraryUnload(l);
     }
     free_reset_buffers();
     if (tile_ctr) cudaFree(tile_ctr);
@@ -165,8 +167,9 @@ struct ff_ctx {
     ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize");  // host buffers go out of scope
   }
 
-  cudaLibrary_t load(int sweep, int ksel) {
-    std::vector<char> cubin = ff::compile_cubin(ff::emit_source(sys, sweep, ksel), "fireflies_system.cu");
+  cudaLibrary_t load(int sweep, int ksel, bool bal = true) {
+    std::vector<char> cubin =
+        ff::compile_cubin(ff::emit_source(sys, sweep, ksel, nullptr, bal), "fireflies_system.cu");
     cudaLibrary_t lib = nullptr;
     ck(cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
     return lib;
@@ -184,22 +187,25 @@ struct ff_ctx {
     return modules.emplace(sweep, m).first->second;
   }
 
-  // step kernel `id` (0-17) of the variant, compiled at its first launch
-  cudaKernel_t step_kernel(Module& m, int sweep, int id) {
-    if (!m.step[id]) {
-      m.step_lib[id] = load(sweep, id);
+  // step kernel `id` (0-11) of the variant, compiled at its first launch
+  cudaKernel_t step_kernel(Module& m, int sweep, int id, bool bal) {
+    if (!m.step[bal][id]) {
+      m.step_lib[bal][id] = load(sweep, id, bal);
       const std::string name = std::string(kStepNames[id % kNumStep]) + (id >= kNumStep ? "_c" : "");
-      ck(cudaLibraryGetKernel(&m.step[id], m.step_lib[id], name.c_str()), "cudaLibraryGetKernel(ff_step)");
+      ck(cudaLibraryGetKernel(&m.step[bal][id], m.step_lib[bal][id], name.c_str()), "cudaLibraryGetKernel(ff_step)");
       int occ = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m.step[id], kStepTPB[id % kNumStep], 0) !=
-          cudaSuccess) {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m.step[bal][id], kStepTPB[id % kNumStep],
+                                                        0) != cudaSuccess) {
         cudaGetLastError();
         occ = 1;
       }
-      m.occ[id] = occ > 0 ? occ : 1;
+      m.occ[bal][id] = occ > 0 ? occ : 1;
     }
-    return m.step[id];
+    return m.step[bal][id];
   }
+  // pipe-balanced (throughput) kernels for launches that fill the GPU; a launch with fewer tiles than
+  // two per SM is latency-bound (one particle's RK4 chain is the critical path) and uses MUFU only
+  bool balanced_for(int64_t ntiles) const { return ntiles >= 2 * (int64_t)nsm; }
 
   // the uniform factors of the split components of a system variant, in slot order (cached)
   std::map<int, std::vector<ff::NodeP>> scale_cache;
@@ -214,13 +220,14 @@ struct ff_ctx {
   }
 
   // host program of the RHS's loop-invariant values of a system variant (cached)
-  std::map<int, ff::UProgram> prog_cache;
-  const ff::UProgram& uprogram(int sweep) {
-    auto it = prog_cache.find(sweep);
+  std::map<std::pair<int, bool>, ff::UProgram> prog_cache;
+  const ff::UProgram& uprogram(int sweep, bool bal) {
+    auto key = std::make_pair(sweep, bal);
+    auto it = prog_cache.find(key);
     if (it != prog_cache.end()) return it->second;
     ff::UProgram prog;
-    ff::emit_source(sys, sweep, 100, &prog);
-    return prog_cache.emplace(sweep, prog).first->second;
+    ff::emit_source(sys, sweep, 100, &prog, bal);
+    return prog_cache.emplace(key, prog).first->second;
   }
 
   int find_param(const char* name) const {
@@ -333,12 +340,13 @@ struct ff_ctx {
       g.sw_val = sweep_param >= 0 ? params[sweep_param] : 0.0f;
     }
     for (size_t k = 0; k < params.size(); ++k) a.p[k] = params[k];
-    {
-      const std::vector<float> q = ff::eval_program(uprogram(sweep_param), params);
-      for (size_t k = 0; k < q.size(); ++k) a.q[k] = q[k];
-    }
     const int64_t tile = (int64_t)p * t;
     const int64_t ntiles = next_slot / tile;
+    const bool bal = balanced_for(ntiles);
+    {
+      const std::vector<float> q = ff::eval_program(uprogram(sweep_param, bal), params);
+      for (size_t k = 0; k < q.size(); ++k) a.q[k] = q[k];
+    }
     if (ntiles == 0) {
       if (xworld) launch_exchange(m);  // this rank has no particles; its peers still wait for it
       return;
@@ -347,8 +355,8 @@ struct ff_ctx {
     const bool colour = image && colour_img;
     const size_t dyn_smem = colour ? 3 * 1024 * sizeof(uint32_t) : 0;
     const int kid = si + (colour ? kNumStep : 0);
-    const cudaKernel_t kern = step_kernel(m, sweep_param, kid);
-    int occ = m.occ[kid];
+    const cudaKernel_t kern = step_kernel(m, sweep_param, kid, bal);
+    int occ = m.occ[bal][kid];
     if (colour) {
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)kern, t, dyn_smem) != cudaSuccess) {
         cudaGetLastError();
@@ -926,7 +934,7 @@ ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* pee
   int pp, tt;
   ctx->default_launch(pp, tt);
   Module& m = ctx->module(ctx->sweep_param);
-  ctx->step_kernel(m, ctx->sweep_param, step_index(pp, tt));
+  ctx->step_kernel(m, ctx->sweep_param, step_index(pp, tt), ctx->balanced_for(ctx->next_slot / ((int64_t)pp * tt)));
   // and force the (lazily loaded) exchange kernel in now: a lazy load at its first launch can wait
   // for the device while a peer's exchange kernel spins waiting for this rank (deadlock on one GPU)
   cudaFuncAttributes fa;
