@@ -934,7 +934,7 @@ ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* pee
   int pp, tt;
   ctx->default_launch(pp, tt);
   Module& m = ctx->module(ctx->sweep_param);
-  ctx->step_kernel(m, ctx->sweep_param, step_index(pp, tt), ctx->balanced_for(ctx->next_slot / ((int64_t)pp * tt)));
+  for (int bal = 0; bal < 2; ++bal) ctx->step_kernel(m, ctx->sweep_param, step_index(pp, tt), bal != 0);
   // and force the (lazily loaded) exchange kernel in now: a lazy load at its first launch can wait
   // for the device while a peer's exchange kernel spins waiting for this rank (deadlock on one GPU)
   cudaFuncAttributes fa;

@@ -130,3 +130,32 @@ def test_null_context_rejected():
     assert L.ff_sync(None) == _abi.FF_ERR_INVALID_ARG
     assert b"ctx is NULL" in L.ff_last_error()
     assert L.ff_destroy(None) == _abi.FF_OK
+
+
+def test_uniform_values_beyond_the_parameter_block_table_still_compile():
+    """More loop-invariant values than FFStepArgs::q holds (FF_MAX_DERIVED = 192): the rest are
+    computed in the kernel as before; the source still compiles to an sm_100a CUBIN."""
+    from paper_1505_00344_b200.systems import SystemDef
+    n = 100
+    params = [(f"p{k}", 1.0 + k * 1e-3, None, None) for k in range(n)]
+    terms = " + ".join(f"p{k}*p{(k + 1) % n}*x + p{k}*p{(k + 2) % n}*x*x" for k in range(n))   # 200 products
+    s = SystemDef("many", ["x"], [terms], params)
+    src = FF.ff_emit_source(s)
+    assert "a.q[191]" in src and "a.q[192]" not in src
+    assert "const float u" in src                  # the overflow values, computed per thread
+    cub = FF.ff_compile_cubin(s)
+    assert cub[:4] == b"\x7fELF"
+
+
+def test_uniform_factor_slots_and_sweep():
+    """Components with a parameter-only factor are split (at most 4 slots); a factor that is the
+    swept parameter stays in the RHS (it is per particle)."""
+    src = FF.ff_emit_source(systems.lorenz())
+    assert "FF_SSLOT[FF_DIM] = {0, -1, -1}" in src          # sigma (y - x)
+    src = FF.ff_emit_source(systems.lorenz(), sweep_param=0)
+    assert "FF_SSLOT[FF_DIM] = {-1, -1, -1}" in src         # sigma swept: not factored
+    src = FF.ff_emit_source(systems.hh_ring(3))
+    m = re.search(r"FF_SSLOT\[FF_DIM\] = \{([^}]*)\}", src)
+    slots = [int(v) for v in m.group(1).split(",")]
+    assert [slots[i] for i in (0, 5, 10)] == [0, 1, 2]       # dV/dt = (...)/C for the 3 neurons
+    assert all(v == -1 for i, v in enumerate(slots) if i not in (0, 5, 10))
