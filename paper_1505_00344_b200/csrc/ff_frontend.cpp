@@ -230,10 +230,99 @@ void factors(const NodeP& n, int sp, std::vector<NodeP>& uni, std::vector<NodeP>
   }
 }
 
+std::string ast_key(const NodeP& n) {  // structural key of an expression
+  std::ostringstream o;
+  o << (int)n->op << ':' << n->index << ':' << n->name << ':';
+  {
+    uint64_t bits;
+    std::memcpy(&bits, &n->value, 8);
+    o << bits;
+  }
+  o << '(';
+  for (const NodeP& a : n->args) o << ast_key(a) << ',';
+  o << ')';
+  return o.str();
+}
+
 NodeP product(const std::vector<NodeP>& f) {
   NodeP p = f[0];
   for (size_t i = 1; i < f.size(); ++i) p = mk(Op::Mul, {p, f[i]});
   return p;
+}
+
+// ---- collecting a state variable out of a sum of driving-force terms
+// Conductance equations are sums of c_i (E_i - V) (each ionic and synaptic current
+// of the HH ring). Written out, every term costs a subtraction and an FFMA with three per-particle
+// register operands (the slow form); collected, sum c_i (E_i - V) = sum c_i E_i -
+// V sum c_i is a chain of FFMAs with uniform operands and one final product. Exact in real arithmetic.
+void sum_terms(const NodeP& n, int sign, std::vector<std::pair<int, NodeP>>& out) {
+  if (n->op == Op::Add) { sum_terms(n->args[0], sign, out); sum_terms(n->args[1], sign, out); }
+  else if (n->op == Op::Sub) { sum_terms(n->args[0], sign, out); sum_terms(n->args[1], -sign, out); }
+  else if (n->op == Op::Neg) sum_terms(n->args[0], -sign, out);
+  else out.push_back({sign, n});
+}
+void prod_factors(const NodeP& n, int& sign, std::vector<NodeP>& out) {
+  if (n->op == Op::Mul) { prod_factors(n->args[0], sign, out); prod_factors(n->args[1], sign, out); }
+  else if (n->op == Op::Neg) { sign = -sign; prod_factors(n->args[0], sign, out); }
+  else out.push_back(n);
+}
+// factor (a - V) or (V - a) with V a state variable and a free of state variables: V's index, a, and
+// the orientation (+1 for a - V)
+bool driving_force(const NodeP& f, int sp, int& var, NodeP& a, int& orient) {
+  if (f->op != Op::Sub) return false;
+  const NodeP &l = f->args[0], &r = f->args[1];
+  if (r->op == Op::Var && param_only(l, sp)) { var = r->index; a = l; orient = 1; return true; }
+  if (l->op == Op::Var && param_only(r, sp)) { var = l->index; a = r; orient = -1; return true; }
+  return false;
+}
+NodeP signed_sum(const std::vector<std::pair<int, NodeP>>& t) {
+  NodeP acc;
+  for (const auto& e : t) {
+    if (!acc) acc = e.first > 0 ? e.second : mk(Op::Neg, {e.second});
+    else acc = mk(e.first > 0 ? Op::Add : Op::Sub, {acc, e.second});
+  }
+  return acc ? acc : mk(Op::Num, {}, 0.0);
+}
+NodeP collect_linear(const NodeP& root, int sp) {
+  std::vector<std::pair<int, NodeP>> terms;
+  sum_terms(root, 1, terms);
+  std::map<int, std::vector<size_t>> by_var;
+  std::vector<int> var(terms.size(), -1), orient(terms.size(), 0);
+  std::vector<NodeP> a(terms.size()), c(terms.size());
+  for (size_t i = 0; i < terms.size(); ++i) {
+    int sign = terms[i].first;
+    std::vector<NodeP> f;
+    prod_factors(terms[i].second, sign, f);
+    for (size_t j = 0; j < f.size(); ++j) {
+      int v, o;
+      NodeP av;
+      if (!driving_force(f[j], sp, v, av, o)) continue;
+      std::vector<NodeP> rest;
+      for (size_t k = 0; k < f.size(); ++k) if (k != j) rest.push_back(f[k]);
+      var[i] = v; a[i] = av; orient[i] = o * sign;   // term = orient * c * (a - V)
+      c[i] = rest.empty() ? mk(Op::Num, {}, 1.0) : product(rest);
+      by_var[v].push_back(i);
+      break;
+    }
+  }
+  std::vector<std::pair<int, NodeP>> out;
+  std::vector<char> done(terms.size(), 0);
+  for (auto& kv : by_var) {
+    if (kv.second.size() < 2) continue;
+    std::vector<std::pair<int, NodeP>> gsum;
+    for (size_t i : kv.second) {
+      out.push_back({orient[i], mk(Op::Mul, {c[i], a[i]})});   // sum c_i E_i
+      gsum.push_back({orient[i], c[i]});
+      done[i] = 1;
+    }
+    NodeP V = std::make_shared<Node>();
+    V->op = Op::Var;
+    V->index = kv.first;
+    out.push_back({-1, mk(Op::Mul, {V, signed_sum(gsum)})});  // - V sum c_i
+  }
+  if (out.empty()) return root;
+  for (size_t i = 0; i < terms.size(); ++i) if (!done[i]) out.push_back(terms[i]);
+  return signed_sum(out);
 }
 
 }  // namespace
@@ -242,16 +331,26 @@ std::vector<int> split_scales(const System& s, int sweep_param, std::vector<Node
   std::vector<int> slot(s.dim, -1);
   rest->assign(s.rhs.begin(), s.rhs.end());
   scale->assign(s.dim, nullptr);
-  int used = 0;
-  for (int d = 0; d < s.dim && used < FF_MAX_SCALED; ++d) {
+  // components with the same factor share a slot (HH ring: dV_i/dt = (...)/C for every neuron), so
+  // the kernel keeps fewer loop-invariant step constants in uniform registers
+  std::map<std::string, int> seen;
+  std::vector<NodeP> first;
+  for (int d = 0; d < s.dim; ++d) {
     std::vector<NodeP> uni, var;
     factors(s.rhs[d], sweep_param, uni, var);
     if (uni.empty() || var.empty()) continue;  // nothing to factor out, or a constant derivative
     // a lone -1 is left to the sign selection (free there)
     if (uni.size() == 1 && uni[0]->op == Op::Num && uni[0]->value == -1.0) continue;
+    const NodeP sc = product(uni);
+    const std::string key = ast_key(sc);
+    auto it = seen.find(key);
+    if (it == seen.end()) {
+      if ((int)seen.size() >= FF_MAX_SCALED) continue;
+      it = seen.emplace(key, (int)seen.size()).first;
+    }
     (*rest)[d] = product(var);
-    (*scale)[d] = product(uni);
-    slot[d] = used++;
+    (*scale)[d] = sc;
+    slot[d] = it->second;
   }
   return slot;
 }
@@ -1036,7 +1135,7 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   Dag g(sweep_param);
   g.plan = &plan;
   std::vector<int> roots;
-  for (int i = 0; i < s.dim; ++i) roots.push_back(g.lower(rest[i]));
+  for (int i = 0; i < s.dim; ++i) roots.push_back(g.lower(collect_linear(rest[i], sweep_param)));
 
   // reachable nodes in topological (creation) order
   std::vector<char> live(g.nodes.size(), 0);

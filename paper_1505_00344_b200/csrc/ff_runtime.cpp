@@ -215,7 +215,10 @@ struct ff_ctx {
     std::vector<ff::NodeP> rest, sc, out;
     const std::vector<int> slot = ff::split_scales(sys, sweep, &rest, &sc);
     for (int d = 0; d < sys.dim; ++d)
-      if (slot[d] >= 0) out.push_back(sc[d]);
+      if (slot[d] >= 0) {
+        if ((int)out.size() <= slot[d]) out.resize(slot[d] + 1);
+        out[slot[d]] = sc[d];   // components sharing a factor share its slot
+      }
     return scale_cache.emplace(sweep, out).first->second;
   }
 

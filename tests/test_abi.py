@@ -157,5 +157,5 @@ def test_uniform_factor_slots_and_sweep():
     src = FF.ff_emit_source(systems.hh_ring(3))
     m = re.search(r"FF_SSLOT\[FF_DIM\] = \{([^}]*)\}", src)
     slots = [int(v) for v in m.group(1).split(",")]
-    assert [slots[i] for i in (0, 5, 10)] == [0, 1, 2]       # dV/dt = (...)/C for the 3 neurons
+    assert [slots[i] for i in (0, 5, 10)] == [0, 0, 0]       # dV/dt = (...)/C: one shared slot
     assert all(v == -1 for i, v in enumerate(slots) if i not in (0, 5, 10))

@@ -60,7 +60,7 @@ def test_front_end_op_counts():
     -> a - (a+b)X for the 12 gating equations)."""
     import bench
     assert bench.op_counts(systems.lorenz(), -1) == (45, 0, 0, 41, 0)
-    assert bench.op_counts(systems.hh_ring(3), -1) == (813, 84, 36, 765, 84)
+    assert bench.op_counts(systems.hh_ring(3), -1) == (813, 84, 36, 741, 84)
     # STN-GPe is MUFU-bound: one of its two sigmoid exponentials per evaluation moves to the FMA pipe
     assert bench.op_counts(systems.stn_gpe(), -1) == (62, 16, 8, 86, 12)
 
