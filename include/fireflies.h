@@ -265,6 +265,7 @@ ff_status ff_sync(ff_ctx* ctx);
  * sum into every rank's image, then a second barrier. When it completes, the bound image equals the
  * element-wise sum over ranks of the images each rank's launch produced alone -- bit-exact, integer
  * -- i.e. ff_step followed by an all-reduce (previous contents included: zero the image per frame).
+ * With world = 1 the image already is the sum and no exchange kernel is launched.
  *   peer_images[p]   DEVICE pointer, valid in THIS process, to rank p's bound uint32 [C][H][W] image
  *                    (16-byte aligned; peer_images[rank] must be the image bound here with ff_project;
  *                    all ranks bind the same C, H, W). Typically symmetric memory mapped over

@@ -351,7 +351,7 @@ struct ff_ctx {
       for (size_t k = 0; k < q.size(); ++k) a.q[k] = q[k];
     }
     if (ntiles == 0) {
-      if (xworld) launch_exchange(m);  // this rank has no particles; its peers still wait for it
+      if (xworld > 1) launch_exchange(m);  // this rank has no particles; its peers still wait for it
       return;
     }
     // position-linear colour: 3 extra per-block table planes in dynamic shared memory
@@ -374,7 +374,7 @@ struct ff_ctx {
     ck(cudaLaunchKernel((const void*)kern, dim3(grid), dim3(t), args, dyn_smem, stream), "launch ff_step");
     tile_base += (uint64_t)ntiles + grid;  // each block fetches until it sees a tile >= ntiles
     ++launches;
-    if (xworld && image) launch_exchange(m);
+    if (xworld > 1 && image) launch_exchange(m);  // (one rank: its image already is the sum)
   }
 
   // the image exchange after a binning launch (ff_set_exchange; ff_device.cuh "image exchange")
