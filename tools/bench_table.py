@@ -18,7 +18,8 @@ def main():
         cb = d.get("cpu_baseline") or {}
         name = os.path.basename(f)[:-5]
         rows.append((name, c.get("particles_per_gpu"), c.get("steps_per_frame"), d["value"], d["ms_per_step"],
-                     r["pipe"], r["frac"], r.get("alg_per_particle_step"), r.get("generated_fma_ops_per_particle_step"),
+                     r["pipe"], r["frac"], r.get("alg_per_particle_step"),
+                     (r.get("work") or {}).get("generated_fma_ops", r.get("generated_fma_ops_per_particle_step")),
                      cb.get("value"), cb.get("cores"), d.get("clocks", {}).get("sm_mhz"),
                      (d.get("e2e") or {}).get("value")))
     lines = ["| workload | particles | steps/launch | particle-steps/s | ms per frame | binding pipe | fraction of peak "
@@ -26,7 +27,7 @@ def main():
              "| SM MHz |", "|---" * 12 + "|"]
     for (n, p, s, v, ms, pipe, frac, alg, gen, cv, cores, mhz, e2e) in rows:
         ratio = f"{v / cv:.0f}x" if cv else "-"
-        ops = f"{alg} / {gen}" if pipe == "fma" else (f"{alg}" if alg is not None else "-")
+        ops = f"{alg:g} / {gen}" if pipe in ("fma", "fma+xu") and gen else (f"{alg:g}" if alg is not None else "-")
         lines.append(f"| {n} | {p:,} | {s} | {v:.3g} | {ms:.3f} | {pipe} | {100 * frac:.1f}% | {ops} | "
                      f"{f'{e2e:.3g}' if e2e else '-'} | {f'{cv:.3g} ({cores})' if cv else '-'} | {ratio} | "
                      f"{mhz if mhz else '-'} |")
