@@ -84,3 +84,75 @@ def rk4_numpy(fns, vars_, pvals, x0, h, n):
         k4 = f(x + h * k3)
         x = x + h / 6 * (k1 + 2 * k2 + 2 * k3 + k4)
     return x
+
+
+def gen_structured(seed):
+    """Random systems built from the forms the front end rewrites: kinetic gating
+    a (1 - x) - b x, driving-force sums sum c_i (E_i - V) in either orientation, parameter-only
+    factors (products, divisions by parameters, negation). Returns the gen_system tuple."""
+    rng = np.random.default_rng(1000 + seed)
+    dim = int(rng.integers(3, 6))
+    vars_ = [f"x{i}" for i in range(dim)]
+    params = [f"p{k}" for k in range(4)]
+    pvals = {p: float(np.round(rng.uniform(0.5, 2.0), 3)) for p in params}
+    texts, fns = [], []
+
+    def var():
+        v = vars_[rng.integers(dim)]
+        return v, (lambda e, v=v: e[v])
+
+    def pos_term():   # a positive-ish varying coefficient
+        v, fv = var()
+        k = int(rng.integers(3))
+        if k == 0:
+            return f"sigmoid({v})", (lambda e: 1 / (1 + math.exp(-fv(e))))
+        if k == 1:
+            return f"exp(0.2*tanh({v}))", (lambda e: math.exp(0.2 * math.tanh(fv(e))))
+        return f"({v})^2", (lambda e: fv(e) ** 2)
+
+    def uni():        # a parameter-only factor
+        p = params[rng.integers(4)]
+        k = int(rng.integers(3))
+        if k == 0:
+            return p, (lambda e, p=p: e[p])
+        if k == 1:
+            q = params[rng.integers(4)]
+            return f"{p}*{q}", (lambda e, p=p, q=q: e[p] * e[q])
+        return f"(1.5 - {p})", (lambda e, p=p: 1.5 - e[p])
+
+    for i in range(dim):
+        form = int(rng.integers(3))
+        x = vars_[i]
+        if form == 0:     # gating: a (1 - x) - b x  (either order)
+            (a, fa), (b, fb) = pos_term(), pos_term()
+            if rng.random() < 0.5:
+                t, f = f"({a})*(1 - {x}) - ({b})*{x}", (lambda e, fa=fa, fb=fb, x=x: fa(e) * (1 - e[x]) - fb(e) * e[x])
+            else:
+                t, f = f"-{x}*({b}) + (1 - {x})*({a})", (lambda e, fa=fa, fb=fb, x=x: -e[x] * fb(e) + (1 - e[x]) * fa(e))
+        elif form == 1:   # driving forces on one variable V, 2-4 terms, both orientations
+            V = vars_[rng.integers(dim)]
+            parts, fs = [], []
+            for _ in range(int(rng.integers(2, 5))):
+                (c, fc), (u, fu) = pos_term(), uni()
+                if rng.random() < 0.5:
+                    parts.append(f"({c})*({u} - {V})")
+                    fs.append(lambda e, fc=fc, fu=fu, V=V: fc(e) * (fu(e) - e[V]))
+                else:
+                    parts.append(f"- ({V} - {u})*({c})")
+                    fs.append(lambda e, fc=fc, fu=fu, V=V: -(e[V] - fu(e)) * fc(e))
+            t = " + ".join(parts) + " + p0"
+            f = (lambda e, fs=tuple(fs): sum(g(e) for g in fs) + e["p0"])
+        else:             # a plain nonlinear term
+            (a, fa), (b, fb) = pos_term(), var()
+            t, f = f"({a}) - {b}*{x}", (lambda e, fa=fa, fb=fb, x=x: fa(e) - fb(e) * e[x])
+        k = int(rng.integers(4))          # parameter-only factor of the whole component
+        if k == 1:
+            t, f = f"({t})/{params[1]}", (lambda e, f=f: f(e) / e["p1"])
+        elif k == 2:
+            (u, fu) = uni()
+            t, f = f"{u}*({t})", (lambda e, f=f, fu=fu: fu(e) * f(e))
+        elif k == 3:
+            t, f = f"-({t})*p2", (lambda e, f=f: -f(e) * e["p2"])
+        texts.append(t)
+        fns.append(f)
+    return vars_, texts, fns, params, pvals
