@@ -432,9 +432,17 @@ def main():
         return
 
     import torch
+    # FF_BENCH_DIST_BACKEND=gloo with FF_BENCH_ONE_DEVICE=1: every rank on cuda:0 -- exercises the
+    # N > 1 code path on a one-GPU box (plumbing check only; its timings mean nothing)
+    backend = os.environ.get("FF_BENCH_DIST_BACKEND", "nccl")
+    if os.environ.get("FF_BENCH_ONE_DEVICE") == "1":
+        local_rank = 0
     if world > 1:
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            torch.distributed.init_process_group(backend)
     device = torch.device("cuda", local_rank)
     torch.cuda.set_device(device)
     r = run_ours(args, w, rank, world, device)
