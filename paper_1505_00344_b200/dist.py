@@ -71,11 +71,32 @@ def peer_tables(buffer_ptrs, C_, H, W):
     return [int(p) for p in buffer_ptrs], [int(p) + sig_off for p in buffer_ptrs]
 
 
-def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=60000.0):
-    """Bind a symmetric-memory image to `ctx` and turn on the fused in-launch image exchange: from
-    now on every ff_step of every rank ends with the image summed over all ranks (no separate
-    collective). Collective over `group` (default: the world); returns the bound image tensor
-    [C][H][W] (int32, zeroed). Needs one GPU per rank with peer access (NVLink / NVSwitch)."""
+def _map_symmetric(buf, group):
+    """torch symmetric memory: (buffer pointers of every rank, rank, world, keepalive)."""
+    import torch.distributed._symmetric_memory as symm_mem
+    handle = symm_mem.rendezvous(buf, group)
+    return list(handle.buffer_ptrs), handle.rank, handle.world_size, handle
+
+
+def _map_ipc(buf, group):
+    """CUDA IPC (the mechanism torch.multiprocessing uses for CUDA tensors): every rank exports its
+    buffer, opens the others'. Works across GPUs with peer access and between processes sharing one
+    GPU (where torch symmetric memory refuses). Returns the same tuple as _map_symmetric."""
+    from torch.multiprocessing.reductions import reduce_tensor
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    rebuild, args = reduce_tensor(buf)
+    shared = [None] * world
+    dist.all_gather_object(shared, (rebuild, args), group=group)
+    peers = [buf if r == rank else fn(*a) for r, (fn, a) in enumerate(shared)]
+    return [t.data_ptr() for t in peers], rank, world, peers
+
+
+def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=60000.0, mapping="auto"):
+    """Bind a peer-accessible image to `ctx` and turn on the library's image exchange: from now on
+    every binning ff_step of every rank is followed, on its stream, by the sum of the images over all
+    ranks (ff_set_exchange; no separate collective). Collective over `group` (default: the world);
+    returns the bound image tensor [C][H][W] (int32, zeroed). mapping: "symmetric" (torch symmetric
+    memory), "ipc" (CUDA IPC handles), "auto" (symmetric, else IPC)."""
     words, sig_off, total = exchange_layout(C_, H, W)
     if not dist.is_initialized() or dist.get_world_size(group) == 1:   # one rank: its own tables
         buf = torch.zeros(total, dtype=torch.int32, device=ctx.device)
@@ -87,17 +108,30 @@ def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=600
         ctx.set_exchange(0, 1, imgs, sigs, timeout_ms)
         ctx._symm = (buf,)
         return image
-    import torch.distributed._symmetric_memory as symm_mem
     group = group if group is not None else dist.group.WORLD
-    buf = symm_mem.empty(total, dtype=torch.int32, device=ctx.device)
-    buf.zero_()
-    handle = symm_mem.rendezvous(buf, group)
+    mapped = None
+    if mapping in ("auto", "symmetric"):
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+            buf = symm_mem.empty(total, dtype=torch.int32, device=ctx.device)
+            buf.zero_()
+            mapped = _map_symmetric(buf, group)
+        except RuntimeError:
+            if mapping == "symmetric":
+                raise
+            mapped = None
+    if mapped is None:
+        buf = torch.zeros(total, dtype=torch.int32, device=ctx.device)
+        torch.cuda.synchronize(ctx.device)
+        mapped = _map_ipc(buf, group)
+    ptrs, rank, world, keep = mapped
     image = buf[:words].view(C_, H, W)
     ctx.project(axes, view, W, H, C_, image=image)   # binds (and bins the current state locally)
     image.zero_()
+    buf[words:].zero_()
     torch.cuda.synchronize(ctx.device)
     dist.barrier(group)                                # every rank's signals are zero
-    imgs, sigs = peer_tables(handle.buffer_ptrs, C_, H, W)
-    ctx.set_exchange(handle.rank, handle.world_size, imgs, sigs, timeout_ms)
-    ctx._symm = (buf, handle)                          # keep the mapping alive with the context
+    imgs, sigs = peer_tables(ptrs, C_, H, W)
+    ctx.set_exchange(rank, world, imgs, sigs, timeout_ms)
+    ctx._symm = (buf, keep)                            # keep the mappings alive with the context
     return image
