@@ -160,16 +160,50 @@ def setup(args, w, rank, world):
     if w.get("prerun"):
         ctx.step(w["prerun"], w["dt"])
     axes, view = projection(w)
-    fused = args.exchange == "fused" and not args.no_image
-    if fused:   # the image sum over ranks happens inside ff_step (ff_set_exchange), no NCCL call
+    fused = not args.no_image and (args.exchange == "fused" or (args.exchange == "auto" and world > 1))
+    img = None
+    if fused:   # the image sum over ranks is done by the library after each launch, no NCCL call
         from paper_1505_00344_b200 import dist as ffdist
-        img = ffdist.bind_exchanged_image(ctx, axes, view, w["W"], w["H"], w["C"])
-    else:
+        try:
+            img = ffdist.bind_exchanged_image(ctx, axes, view, w["W"], w["H"], w["C"])
+            if args.exchange == "auto":
+                ok, why = validate_exchange(ctx, img, w)
+                if not ok:
+                    raise RuntimeError(why)
+        except Exception as e:   # auto: fall back to the NCCL all-reduce, say why in the line
+            if args.exchange == "fused":
+                raise
+            args.exchange_note = f"library exchange unavailable ({str(e)[:160]}); NCCL all-reduce used"
+            ctx.set_exchange(0, 0)
+            fused, img = False, None
+    if img is None:
         img = ctx.project(axes, view, w["W"], w["H"], w["C"])
     if args.no_image:   # integration only (HBM roofline of single-step launches without binning)
         ctx.unbind_image()
     torch.cuda.synchronize()
     return ctx, gids, img, fused
+
+
+def validate_exchange(ctx, img, w):
+    """One bin-only frame through the library exchange: it must complete (ff_sync) and leave the same
+    image on every rank (checksums compared with MIN / MAX all-reduces)."""
+    import torch
+    img.zero_()
+    ctx.step(0, w["dt"])
+    try:
+        ctx.sync()
+    except Exception as e:
+        return False, f"exchange frame failed: {e}"
+    v = img.to(torch.float64).flatten()
+    wts = torch.arange(1, v.numel() + 1, dtype=torch.float64, device=v.device) % 1009
+    ck = torch.stack([v.sum(), (v * wts).sum()])
+    lo, hi = ck.clone(), ck.clone()
+    torch.distributed.all_reduce(lo, op=torch.distributed.ReduceOp.MIN)
+    torch.distributed.all_reduce(hi, op=torch.distributed.ReduceOp.MAX)
+    if not torch.equal(lo, hi) or float(lo[0]) <= 0:
+        return False, "ranks' exchanged images differ"
+    img.zero_()
+    return True, ""
 
 
 def run_ours(args, w, rank, world, device):
@@ -301,7 +335,7 @@ def run_ours(args, w, rank, world, device):
     if "sweep" in w:
         sweep_idx = [p[0] for p in make_system(w["system"]).params].index(w["sweep"][0])
     return dict(S=S, n_total=n_total, n_local=n_local, sweep_idx=sweep_idx, t_total_ms=t_total, kern_ms=kern_mean,
-                frame_ms=frame_ms, launches=launches, clocks=clk.summary(), e2e=e2e, image_sum=im_sum,
+                frame_ms=frame_ms, launches=launches, clocks=clk.summary(), e2e=e2e, image_sum=im_sum, fused=fused,
                 t_wall=t_wall)
 
 
@@ -392,9 +426,10 @@ def main():
     ap.add_argument("--flush", default="read", choices=["read", "memset", "none"],
                     help="L2 flush between timed frames (default: read 256 MiB; 'none' only for experiments)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
-                    help="per-frame image sum over ranks: NCCL all-reduce after the launch, or fused into "
-                         "the launch over peer memory (ff_set_exchange)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "fused"],
+                    help="per-frame image sum over ranks (N > 1): the library's exchange over peer memory "
+                         "after each launch (ff_set_exchange; 'auto' validates it once and falls back to NCCL), "
+                         "or an NCCL all-reduce")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = WORKLOADS[args.config]
@@ -405,10 +440,7 @@ def main():
     config = {"workload": args.config, "description": w["desc"], "steps_per_frame": S, "dt": w["dt"],
               "particles_per_gpu": (sum(g[0] for g in w["groups"]) // (world if w.get("strong") else 1)),
               "image": [w["C"], w["H"], w["W"]], "l2": "flushed between timed frames (256 MiB read, outside the timed events)",
-              "parallelism": (f"particles sharded over {world} GPU(s), " + (
-                  "image sum fused into the step launch over NVLink peer memory" if args.exchange == "fused"
-                  else "NCCL image all-reduce per frame")) if world > 1 else "1 GPU",
-              "exchange": args.exchange}
+              "parallelism": "1 GPU"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -446,6 +478,13 @@ def main():
     device = torch.device("cuda", local_rank)
     torch.cuda.set_device(device)
     r = run_ours(args, w, rank, world, device)
+    if world > 1:
+        config["parallelism"] = f"particles sharded over {world} GPU(s), " + (
+            "image sum by the library's exchange kernel over NVLink peer memory after each launch"
+            if r["fused"] else "NCCL image all-reduce per frame")
+        config["exchange"] = "library" if r["fused"] else "nccl"
+        if getattr(args, "exchange_note", None):
+            config["exchange_note"] = args.exchange_note
     if world > 1:
         torch.distributed.destroy_process_group()
     if rank != 0:

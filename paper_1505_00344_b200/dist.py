@@ -116,7 +116,7 @@ def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=600
             buf = symm_mem.empty(total, dtype=torch.int32, device=ctx.device)
             buf.zero_()
             mapped = _map_symmetric(buf, group)
-        except RuntimeError:
+        except Exception:   # (no symmetric-memory backend for this group / same-device ranks)
             if mapping == "symmetric":
                 raise
             mapped = None
