@@ -10,9 +10,10 @@ perspective density image 1024 x 1024 x 2 channels, S = 100 steps per frame.
                   [--S steps_per_frame] [--impl ours|reference]
 
 Under torchrun (N > 1) every rank runs the same per-rank workload on its shard (weak scaling) and
-the per-frame image is summed with an NCCL all-reduce (the path's one exchange step, SURVEY.md
-8(e)); the time is the max over ranks. --impl reference times the CPU oracle (the tier's reference
-arm) on a bounded sample of the same workload.
+the per-frame image is summed over the ranks (the path's one exchange step) by the
+library's exchange kernel over peer memory (--exchange auto, validated on one frame, else an NCCL
+all-reduce; --exchange nccl|fused forces one); the time is the max over ranks. --impl reference
+times the CPU oracle (the tier's reference arm) on a bounded sample of the same workload.
 """
 import argparse
 import json
