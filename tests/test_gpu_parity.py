@@ -422,3 +422,45 @@ def test_high_dim_system_compiles_and_matches():
     ctx.step(50, 0.01)
     want = oracle_group(O.LINEAR, [-1.0] * n_d, [1.0] * n_d, 7, 0, 1000, A.ravel(), 0.01, 50)
     assert tier_a(ctx.read_state(g), want, np.ones(n_d)) <= 1e-5
+
+
+def test_degenerate_inputs():
+    """Edge cases of the method: dt = 0 leaves the state bit-identical; a shard that holds no particle
+    of a group (world > n) launches, bins nothing and the shards still sum to the whole; a swept group
+    next to an unswept one (the latter uses the parameter's value) both match the oracle."""
+    n = 4096 + 1
+    ctx = lorenz_ctx([n])
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=21)
+    x0 = ctx.read_state(g)
+    ctx.step(7, 0.0)
+    assert np.array_equal(ctx.read_state(g).view(np.uint32), x0.view(np.uint32))
+
+    # world 3, groups of 2 and 1 particles: some shards hold none of a group
+    imgs = []
+    for rank in range(3):
+        c = FF.Context(systems.lorenz(), [2, 1], rank=rank, world=3)
+        c.init_group(LZ_LO, LZ_HI, 2, 1, 0, seed=22)
+        c.init_group(LZ_LO, LZ_HI, 1, -1, 1, seed=23)
+        img = c.project([0, 2], [-20.0, 20.0, 0.0, 50.0], 64, 64, 2)
+        img.zero_()
+        c.step(3, 0.01)
+        imgs.append(c.read_image().astype(np.uint64))
+    whole = np.zeros((2, 64, 64), np.uint64)
+    for seed, n_, h, colour in ((22, 2, 0.01, 0), (23, 1, -0.01, 1)):
+        x = O.rk4(O.LORENZ, O.ic_uniform(LZ_LO, LZ_HI, seed, 0, n_), LZ_P, np.float32(h), 3)
+        whole += O.histogram(x, [0, 2], [-20.0, 20.0, 0.0, 50.0], 64, 64, 2, colour).astype(np.uint64)
+    assert np.array_equal(sum(imgs), whole)
+
+    # swept group + unswept group in one context
+    m = 6000 + 7
+    ctx = lorenz_ctx([m, m], r=20.0)
+    gs = ctx.init_group(LZ_LO, LZ_HI, m, 1, 0, seed=24)
+    gu = ctx.init_group(LZ_LO, LZ_HI, m, 1, 0, seed=25)
+    ctx.sweep_param(gs, "r", 0.0, 40.0, 1)
+    sv = O.sweep_values(0.0, 40.0, 1, 0, 0, m, m)
+    ctx.step(10, 0.01)
+    p = np.array([10.0, 20.0, 8.0 / 3.0], np.float32)
+    want_s = O.rk4(O.LORENZ, O.ic_uniform(LZ_LO, LZ_HI, 24, 0, m), p, np.float32(0.01), 10, 1, sv)
+    want_u = O.rk4(O.LORENZ, O.ic_uniform(LZ_LO, LZ_HI, 25, 0, m), p, np.float32(0.01), 10)
+    assert tier_a(ctx.read_state(gs), want_s, dim_scales(LZ_LO, LZ_HI)) <= 1e-5
+    assert tier_a(ctx.read_state(gu), want_u, dim_scales(LZ_LO, LZ_HI)) <= 1e-5
