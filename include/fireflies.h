@@ -230,6 +230,16 @@ ff_status ff_write_state(ff_ctx* ctx, int group_id, int64_t first, int64_t count
 /* Copy the bound image to a HOST uint32 [C][H][W] buffer (synchronous). */
 ff_status ff_read_image(ff_ctx* ctx, uint32_t* host_image);
 
+/* Stream-ordered variants of ff_write_state / ff_read_image: the copy is queued on the bound stream
+ * and the call returns at once (the host buffer must stay valid -- and for a true asynchronous copy
+ * be page-locked -- until the stream has passed it; synchronise with ff_sync or a stream event).
+ * They let a caller pipeline frames: the next frame's state copy-in and the previous frame's image
+ * copy-out overlap the current frame's integration on another context / stream.
+ * Errors: as the synchronous calls, without the synchronisation. */
+ff_status ff_write_state_async(ff_ctx* ctx, int group_id, int64_t first, int64_t count,
+                               const float* host_soa);
+ff_status ff_read_image_async(ff_ctx* ctx, uint32_t* host_image);
+
 /* Render the bound count image to a displayable RGB frame (sprites with an intensity
  * that falls off with the distance from their centre, coloured per group, blended
  * additively), async on the bound stream:

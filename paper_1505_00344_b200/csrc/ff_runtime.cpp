@@ -811,7 +811,8 @@ ff_status ff_set_launch(ff_ctx* ctx, int ppt, int tpb) {
   FF_CATCH
 }
 
-static void state_copy(ff_ctx* ctx, int group_id, int64_t first, int64_t count, void* host, bool to_host) {
+static void state_copy(ff_ctx* ctx, int group_id, int64_t first, int64_t count, void* host, bool to_host,
+                       bool sync = true) {
   need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
   const GroupRec& g = ctx->group(group_id);
   need(host || count == 0, FF_ERR_INVALID_ARG, "host buffer is NULL");
@@ -826,7 +827,7 @@ static void state_copy(ff_ctx* ctx, int group_id, int64_t first, int64_t count, 
     ck(cudaMemcpy2DAsync(dev, (size_t)ctx->pitch * sizeof(float), host, w, w, ctx->sys.dim, cudaMemcpyHostToDevice,
                          ctx->stream), "cudaMemcpy2DAsync H2D");
   }
-  ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+  if (sync) ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
 }
 
 ff_status ff_read_state(ff_ctx* ctx, int group_id, int64_t first, int64_t count, float* host_soa) {
@@ -878,13 +879,29 @@ ff_status ff_render(ff_ctx* ctx, const float* colours, float intensity, float ra
   FF_CATCH
 }
 
-ff_status ff_read_image(ff_ctx* ctx, uint32_t* host_image) {
-  FF_TRY
+static void image_copy(ff_ctx* ctx, uint32_t* host_image, bool sync) {
   need(ctx && host_image, FF_ERR_INVALID_ARG, "NULL argument");
   need(ctx->image != nullptr, FF_ERR_STATE, "no image bound");
   ck(cudaMemcpyAsync(host_image, ctx->image, (size_t)ctx->W * ctx->H * ctx->C * sizeof(uint32_t),
                      cudaMemcpyDeviceToHost, ctx->stream), "cudaMemcpyAsync D2H image");
-  ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+  if (sync) ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+}
+
+ff_status ff_read_image(ff_ctx* ctx, uint32_t* host_image) {
+  FF_TRY
+  image_copy(ctx, host_image, true);
+  FF_CATCH
+}
+
+ff_status ff_read_image_async(ff_ctx* ctx, uint32_t* host_image) {
+  FF_TRY
+  image_copy(ctx, host_image, false);
+  FF_CATCH
+}
+
+ff_status ff_write_state_async(ff_ctx* ctx, int group_id, int64_t first, int64_t count, const float* host_soa) {
+  FF_TRY
+  state_copy(ctx, group_id, first, count, const_cast<float*>(host_soa), false, false);
   FF_CATCH
 }
 

@@ -157,6 +157,16 @@ def ff_read_image_into(ctx, host_ptr: int):
     check(lib().ff_read_image(ctx, C.c_void_p(host_ptr)))
 
 
+def ff_write_state_async(ctx, group_id: int, first: int, count: int, host_ptr: int):
+    """Stream-ordered copy-in of [dim][count] floats from (pinned) host memory at host_ptr."""
+    check(lib().ff_write_state_async(ctx, group_id, first, count, C.c_void_p(host_ptr)))
+
+
+def ff_read_image_async(ctx, host_ptr: int):
+    """Stream-ordered copy-out of the bound image to (pinned) host memory at host_ptr."""
+    check(lib().ff_read_image_async(ctx, C.c_void_p(host_ptr)))
+
+
 def ff_render(ctx, colours, intensity: float, radius_px: float, dev_rgb_ptr: int):
     col = np.ascontiguousarray(colours, dtype=np.float32)
     check(lib().ff_render(ctx, _fptr(col), intensity, radius_px, C.c_void_p(dev_rgb_ptr)))

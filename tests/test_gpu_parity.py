@@ -464,3 +464,24 @@ def test_degenerate_inputs():
     want_u = O.rk4(O.LORENZ, O.ic_uniform(LZ_LO, LZ_HI, 25, 0, m), p, np.float32(0.01), 10)
     assert tier_a(ctx.read_state(gs), want_s, dim_scales(LZ_LO, LZ_HI)) <= 1e-5
     assert tier_a(ctx.read_state(gu), want_u, dim_scales(LZ_LO, LZ_HI)) <= 1e-5
+
+
+def test_async_state_and_image_copies():
+    """ff_write_state_async / ff_read_image_async: stream-ordered copies equal to the synchronous
+    ones once the stream is synchronised."""
+    from paper_1505_00344_b200 import fireflies as F
+    n = 5000 + 3
+    ctx = lorenz_ctx([n])
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=31)
+    img = ctx.project([0, 2], [-20.0, 20.0, 0.0, 50.0], 64, 48, 1)
+    rng = np.random.default_rng(3)
+    src = torch.from_numpy(rng.uniform(-5, 5, (3, n)).astype(np.float32)).pin_memory()
+    F.ff_write_state_async(ctx.ctx, g, 0, n, src.data_ptr())
+    img.zero_()
+    ctx.step(0, 0.01)                              # bins the state just written (stream order)
+    out = torch.empty((1, 48, 64), dtype=torch.int32).pin_memory()
+    F.ff_read_image_async(ctx.ctx, out.data_ptr())
+    ctx.sync()
+    assert np.array_equal(ctx.read_state(g), src.numpy())
+    assert np.array_equal(out.numpy().view(np.uint32), ctx.read_image())
+    assert np.array_equal(ctx.read_image(), O.histogram(src.numpy(), [0, 2], [-20.0, 20.0, 0.0, 50.0], 64, 48, 1, 0))
