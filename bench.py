@@ -388,6 +388,8 @@ def cpu_oracle_sample(w, n_sample, S):
         names = O.PARAMS[model]
     p = np.array([pvals[k] for k in names], np.float32)
     lo, hi = w["box"]
+    if "sweep" in w:   # swept values exist for the group's own particles only
+        n_sample = min(n_sample, w["groups"][0][0])
     x = O.ic_uniform(lo, hi, w["groups"][0][3], 0, n_sample)
     sweep_idx, sv = -1, None
     if "sweep" in w:
@@ -400,7 +402,7 @@ def cpu_oracle_sample(w, n_sample, S):
     O.histogram(x, axes, view, w["W"], w["H"], w["C"], 0, sweep_vals=sv)
     dt = time.perf_counter() - t0
     threads = int(os.environ.get("OMP_NUM_THREADS", 0)) or len(os.sched_getaffinity(0))
-    return n_sample * S / dt, dt, threads
+    return n_sample * S / dt, dt, threads, n_sample
 
 
 def reference_sample_size(w, S):
@@ -451,7 +453,7 @@ def main():
         for _ in range(args.warmup if args.warmup < 3 else 1):
             cpu_oracle_sample(w, max(256, n // 16), S)
         for _ in range(args.steps if args.steps <= 5 else 5):
-            v, dt, threads = cpu_oracle_sample(w, n, S)
+            v, dt, threads, n = cpu_oracle_sample(w, n, S)
             vals.append(v)
         v = float(np.median(vals))
         sample = f"{n} particles of the workload x {S} RK4 steps + binning per step (oracle, FP32, OpenMP)"
@@ -546,7 +548,7 @@ def main():
             "build": __import__("paper_1505_00344_b200.fireflies", fromlist=["x"]).ff_build_info()}
     if world == 1 and not args.no_cpu_baseline:
         n = reference_sample_size(w, r["S"])
-        v, dt, threads = cpu_oracle_sample(w, n, r["S"])
+        v, dt, threads, n = cpu_oracle_sample(w, n, r["S"])
         line["cpu_baseline"] = {"value": v, "unit": "particle-steps/s", "cores": threads, "kind": "oracle",
                                 "sample": f"{n} particles x {r['S']} RK4 steps + binning ({dt:.1f} s)"}
     print(json.dumps(line))

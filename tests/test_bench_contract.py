@@ -36,3 +36,17 @@ def test_workloads_cover_baseline_configs():
     assert w["hh"]["groups"][0][0] == 1 << 20 and len(w["hh"]["box"][0]) == 15      # configs[2]
     assert w["sweep"]["groups"][0][0] == 1 << 24 and w["sweep"]["sweep"][1:3] == ("r", 0.0, 200.0)[1:]  # configs[3]
     assert w["lorenz1b"]["groups"][0][0] == 1 << 30 and w["lorenz1b"].get("strong")  # configs[4]
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.parametrize("config", ["lorenz3d", "sweep", "stn_bif3d", "hh", "lorenz1b", "lorenz3d_collapsed"])
+def test_reference_arm_runs_every_workload(config):
+    """The oracle sample of every bench workload (swept ones included) runs and prints its line."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "1", "--config", config, "--S", "2"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env=dict(os.environ, FF_BENCH_REF_PARTICLES="2048"))
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([l for l in out.stdout.strip().splitlines() if l.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"] == config
