@@ -50,3 +50,20 @@ def test_reference_arm_runs_every_workload(config):
     assert out.returncode == 0, out.stderr[-2000:]
     d = json.loads([l for l in out.stdout.strip().splitlines() if l.startswith("{")][-1])
     assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"] == config
+
+
+def test_reference_arm_under_torchrun_prints_once():
+    """N > 1 (torchrun): rank 0 alone runs the reference arm and prints its line; the other ranks
+    exit 0 without work."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port),
+                          os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
+                          "--warmup", "1", "--config", "lorenz3d", "--S", "2"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env=dict(os.environ, FF_BENCH_REF_PARTICLES="2048"))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1 and json.loads(lines[0])["n_gpus"] == 2
