@@ -405,6 +405,33 @@ def cpu_oracle_sample(w, n_sample, S):
     return n_sample * S / dt, dt, threads, n_sample
 
 
+def host_cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def single_core_oracle(config, n, S):
+    """The oracle on ONE host core (OMP_NUM_THREADS=1 in a child process): the analogue of the paper's
+    Table 1 "Single Core" column (i5-2500K, gcc -Ofast)."""
+    import subprocess
+    code = ("import sys; sys.argv=['bench']; import bench; "
+            f"v, dt, t, n = bench.cpu_oracle_sample(bench.WORKLOADS[{config!r}], {int(n)}, {int(S)}); "
+            "print(v, dt, n)")
+    try:
+        out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300,
+                             env=dict(os.environ, OMP_NUM_THREADS="1"))
+        v, dt, n = out.stdout.split()
+        return {"value": float(v), "unit": "particle-steps/s", "cores": 1,
+                "sample": f"{int(n)} particles x {S} RK4 steps + binning ({float(dt):.1f} s)"}
+    except Exception as e:   # the baseline is context; never fail the bench line over it
+        return {"error": str(e)[:200]}
+
+
 def reference_sample_size(w, S):
     # bounded sample: ~5-12 s of the oracle on a 16-core host (Lorenz ~5e8, STN-GPe ~1.4e8, HH ring
     # ~3.6e7 particle-steps/s measured), i.e. several frames' worth of the workload's particles
@@ -550,7 +577,9 @@ def main():
         n = reference_sample_size(w, r["S"])
         v, dt, threads, n = cpu_oracle_sample(w, n, r["S"])
         line["cpu_baseline"] = {"value": v, "unit": "particle-steps/s", "cores": threads, "kind": "oracle",
-                                "sample": f"{n} particles x {r['S']} RK4 steps + binning ({dt:.1f} s)"}
+                                "sample": f"{n} particles x {r['S']} RK4 steps + binning ({dt:.1f} s)",
+                                "host_cpu": host_cpu_model(),
+                                "single_core": single_core_oracle(args.config, max(1024, n // 32), r["S"])}
     print(json.dumps(line))
 
 
