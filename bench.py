@@ -338,11 +338,12 @@ def run_ours(args, w, rank, world, device):
 
 
 EXP2P_OPS = 8   # FMA-pipe ops of one exponential computed on the FMA pipe (ff_exp2p in ff_device.cuh)
+PAIR_OPS = 3    # FMA-pipe ops that let two sigmoids share one reciprocal (one MUFU.RCP fewer)
 
 
 def op_counts(sysdef, sweep_idx):
     """Work per particle-step: (algorithmic FMA-pipe lane-ops, algorithmic MUFU ops, exponentials,
-    generated FMA-pipe lane-ops, generated MUFU ops).
+    generated FMA-pipe lane-ops, generated MUFU ops, sigmoid pairs).
 
     Algorithmic = the plain formulation of the system (as written: no gating-form rewrite, every
     uniform factor of dx/dt multiplied in each of the 4 evaluations, every exponential on MUFU) + the
@@ -352,26 +353,29 @@ def op_counts(sysdef, sweep_idx):
     import re
     import paper_1505_00344_b200 as FF
     src = FF.ff_emit_source(sysdef, sweep_idx)
-    m = re.search(r"per evaluation \(front-end count\): (\d+) arithmetic ops, (\d+) MUFU ops", src)
+    m = re.search(r"per particle-step, 4 evaluations \(front-end count\): (\d+) arithmetic ops, (\d+) MUFU ops", src)
     p = re.search(r"plain formulation \(no gating rewrite, uniform factors multiplied in every evaluation\): "
-                  r"(\d+) arithmetic ops, (\d+) MUFU ops, (\d+) exponentials", src)
+                  r"(\d+) arithmetic ops, (\d+) MUFU ops, (\d+) exponentials, (\d+) sigmoid pairs", src)
     return (4 * int(p.group(1)) + 7 * sysdef.dim, 4 * int(p.group(2)), 4 * int(p.group(3)),
-            4 * int(m.group(1)) + 7 * sysdef.dim, 4 * int(m.group(2)))
+            int(m.group(1)) + 7 * sysdef.dim, int(m.group(2)), 4 * int(p.group(4)))
 
 
-def balanced_work(fma_ops, mufu_ops, n_exp):
+def balanced_work(fma_ops, mufu_ops, n_exp, n_pairs=0):
     """FP32-pipe-equivalent work per particle-step of the pipe-balanced roofline: the FMA and MUFU
-    pipes run concurrently (128 and 16 results / clk / SM) and any exponential can move from MUFU to
-    the FMA pipe at EXP2P_OPS ops, so the least time per particle-step on one SM is
-    T = min_k max((mufu - k) / 16, (fma + EXP2P_OPS k) / 128) cycles; work = 128 T lane-ops (= fma
-    for an FMA-bound system). Returns (work, k, binding pipes)."""
-    best = (max(mufu_ops / XU_LANES, fma_ops / FMA_LANES), 0)
-    for k in range(1, n_exp + 1):
-        t = max((mufu_ops - k) / XU_LANES, (fma_ops + EXP2P_OPS * k) / FMA_LANES)
-        if t < best[0] - 1e-12:
-            best = (t, k)
-    t, k = best
-    pipes = "fma" if fma_ops / FMA_LANES >= mufu_ops / XU_LANES and k == 0 else ("xu" if k == 0 else "fma+xu")
+    pipes run concurrently (128 and 16 results / clk / SM); any exponential can move from MUFU to the
+    FMA pipe at EXP2P_OPS ops, and two sigmoids can share one reciprocal for PAIR_OPS ops, so the
+    least time per particle-step on one SM is T = min over k, pairing of
+    max((mufu - pairs - k) / 16, (fma + PAIR_OPS pairs + EXP2P_OPS k) / 128) cycles; work = 128 T
+    lane-ops (= fma for an FMA-bound system). Returns (work, k, binding pipes)."""
+    best = (max(mufu_ops / XU_LANES, fma_ops / FMA_LANES), 0, 0)
+    for pr in ((0, n_pairs) if n_pairs else (0,)):
+        for k in range(0, n_exp + 1):
+            t = max((mufu_ops - pr - k) / XU_LANES, (fma_ops + PAIR_OPS * pr + EXP2P_OPS * k) / FMA_LANES)
+            if t < best[0] - 1e-12:
+                best = (t, k, pr)
+    t, k, pr = best
+    moved = k or pr
+    pipes = "fma" if fma_ops / FMA_LANES >= mufu_ops / XU_LANES and not moved else ("xu" if not moved else "fma+xu")
     return FMA_LANES * t, k, pipes
 
 
@@ -531,8 +535,8 @@ def main():
     # executes 41). The ALU roofline is pipe-balanced (balanced_work): FMA-bound systems report against
     # the FP32 peak as before; a MUFU-bound one against the least time both pipes together need.
     sysdef = make_system(w["system"])
-    fma_ops, mufu_ops, n_exp, gen_ops, gen_mufu = op_counts(sysdef, r["sweep_idx"])
-    work, k_bal, alu_pipes = balanced_work(fma_ops, mufu_ops, n_exp)
+    fma_ops, mufu_ops, n_exp, gen_ops, gen_mufu, n_pairs = op_counts(sysdef, r["sweep_idx"])
+    work, k_bal, alu_pipes = balanced_work(fma_ops, mufu_ops, n_exp, n_pairs)
     dim = sysdef.dim
     cands = {
         "alu": (per_launch * work / kern_s, N_SM * FMA_LANES * f_max,
@@ -550,7 +554,7 @@ def main():
             "unit": unit, "achieved": ach / scale,
             "peak": peak / scale, "frac": ach / peak, "peak_source": src,
             "alg_per_particle_step": per_unit,
-            "work": {"fma_ops": fma_ops, "mufu_ops": mufu_ops, "exponentials": n_exp,
+            "work": {"fma_ops": fma_ops, "mufu_ops": mufu_ops, "exponentials": n_exp, "sigmoid_pairs": n_pairs,
                      "balanced_exponentials_on_fma": k_bal,
                      "generated_fma_ops": gen_ops, "generated_mufu_ops": gen_mufu},
             "fracs_all_pipes": fracs,

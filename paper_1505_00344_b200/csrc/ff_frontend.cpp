@@ -820,6 +820,12 @@ std::string node_expr(const DNode& n, F A) {
 struct Operand { int node; int neg; };
 struct Choice { enum Form { ADD, SUB, FMA, MUL, DIV, OTHER, NEGATE } form; Operand op[3]; };
 
+// host-evaluated loop-invariant values shared by every emitted RHS variant: (node, negate) -> q slot
+struct QTable {
+  std::map<std::pair<int, int>, int> slot;
+  std::vector<std::pair<int, int>> list;
+};
+
 struct SignSelect {
   const Dag& g;
   const std::vector<char>& live;
@@ -832,8 +838,15 @@ struct SignSelect {
 
   std::set<int> emul;  // exponentials computed on the FMA pipe (ff_exp2p) instead of MUFU.EX2
   static constexpr int kExp2pOps = 8;
-  SignSelect(const Dag& dag, const std::vector<char>& lv, const std::vector<int>& roots, std::set<int> em = {})
-      : g(dag), live(lv), uses(dag.nodes.size(), 0), uref(dag.nodes.size()), emul(std::move(em)) {
+  // sigmoid pairs sharing one reciprocal: 1/dA = dB / (dA dB), 1/dB = dA / (dA dB) (pipe balancing)
+  std::map<int, int> pair_of;
+  static constexpr int kPairOps = 3;   // dA dB, dB P, dA P (the clamps run on the ALU pipe)
+  QTable own_q;
+  QTable* qt;
+  SignSelect(const Dag& dag, const std::vector<char>& lv, const std::vector<int>& roots, std::set<int> em = {},
+             std::map<int, int> pairs = {}, QTable* shared_q = nullptr)
+      : g(dag), live(lv), uses(dag.nodes.size(), 0), uref(dag.nodes.size()), emul(std::move(em)),
+        pair_of(std::move(pairs)), qt(shared_q ? shared_q : &own_q) {
     c[0].assign(g.nodes.size(), 0.0);
     c[1].assign(g.nodes.size(), 0.0);
     addsub_uses.assign(g.nodes.size(), 0);
@@ -933,18 +946,41 @@ struct SignSelect {
     return bc;
   }
 
-  // host-evaluated loop-invariant values: (node, negate) -> q slot
-  std::map<std::pair<int, int>, int> qslot;
-  std::vector<std::pair<int, int>> qlist;
+  // host-evaluated loop-invariant values: (node, negate) -> q slot (table shared by the variants)
   std::string qref(int id, int s) {
     auto key = std::make_pair(id, s);
-    auto it = qslot.find(key);
-    if (it != qslot.end()) return "a.q[" + std::to_string(it->second) + "]";
-    if ((int)qlist.size() >= FF_MAX_DERIVED) return "";
-    const int k = (int)qlist.size();
-    qlist.push_back(key);
-    qslot[key] = k;
+    auto it = qt->slot.find(key);
+    if (it != qt->slot.end()) return "a.q[" + std::to_string(it->second) + "]";
+    if ((int)qt->list.size() >= FF_MAX_DERIVED) return "";
+    const int k = (int)qt->list.size();
+    qt->list.push_back(key);
+    qt->slot[key] = k;
     return "a.q[" + std::to_string(k) + "]";
+  }
+
+  // both sigmoids of a pair, computed together; returns the temporary holding node `id`
+  std::string paired_sigmoid(int id) {
+    const int a = std::min(id, pair_of.at(id)), b = std::max(id, pair_of.at(id));
+    auto e = [&](int n) {
+      const std::string u = get(g.nodes[n].a[0], 0);
+      if (emul.count(n)) { n_arith += kExp2pOps; return "ff_exp2p(" + u + ")"; }
+      ++n_mufu;
+      return "ff_exp2(" + u + ")";
+    };
+    const std::string ea = e(a), eb = e(b);
+    const std::string da = "t" + std::to_string(tmp++), db = "t" + std::to_string(tmp++);
+    const std::string pr = "t" + std::to_string(tmp++), sa = "t" + std::to_string(tmp++), sb = "t" + std::to_string(tmp++);
+    // exponentials clamped at 2^60 so the product stays finite (a sigmoid below 1e-18 is 0 here)
+    body << "  const V " << da << " = 1.0f + ff_min(" << ea << ", 1.15292150e18f);\n";
+    body << "  const V " << db << " = 1.0f + ff_min(" << eb << ", 1.15292150e18f);\n";
+    body << "  const V " << pr << " = ff_rcp(" << da << " * " << db << ");\n";
+    body << "  const V " << sa << " = " << db << " * " << pr << ";\n";
+    body << "  const V " << sb << " = " << da << " * " << pr << ";\n";
+    n_arith += 2 + kPairOps;
+    ++n_mufu;
+    memo[{a, 0}] = sa;
+    memo[{b, 0}] = sb;
+    return memo[{id, 0}];
   }
 
   std::string ureference(int id) {
@@ -1003,6 +1039,7 @@ struct SignSelect {
             n_arith += kExp2pOps;
             break;
           }
+          if (n.k == K::Sigmoid2 && pair_of.count(id)) return paired_sigmoid(id);
           if (emul.count(id) && n.k == K::Sigmoid2) {
             e = "ff_rcp(1.0f + ff_exp2p(" + get(n.a[0], 0) + "))";
             n_arith += kExp2pOps + 1;
@@ -1104,7 +1141,7 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   }
   // the plain formulation's op count (no gating rewrite, no factored scales): the fixed algorithmic
   // work per evaluation that bench.py's roofline counts
-  int n_arith_plain = 0, n_mufu_plain = 0, n_exp_plain = 0;
+  int n_arith_plain = 0, n_mufu_plain = 0, n_exp_plain = 0, n_sig_plain = 0;
   {
     Dag gp(sweep_param);
     gp.plan = &plan;
@@ -1126,8 +1163,10 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
     n_arith_plain = sp.n_arith;
     n_mufu_plain = sp.n_mufu;
     for (size_t id = 0; id < gp.nodes.size(); ++id)
-      if (lv[id] && !gp.nodes[id].uniform && (gp.nodes[id].k == K::Exp2 || gp.nodes[id].k == K::Sigmoid2))
+      if (lv[id] && !gp.nodes[id].uniform && (gp.nodes[id].k == K::Exp2 || gp.nodes[id].k == K::Sigmoid2)) {
         ++n_exp_plain;
+        n_sig_plain += gp.nodes[id].k == K::Sigmoid2;
+      }
   }
   // pass 2: lower with the sharing plan; split components are lowered without their uniform factor
   std::vector<NodeP> rest, scale_ast;
@@ -1147,30 +1186,64 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   for (int r : roots) mark(r);
 
   // Pipe balancing: a system bound by the MUFU pipe (16 results / clk / SM against 128 FP32 lanes)
-  // computes some of its exponentials with ff_exp2p on the FMA pipe instead (8 FMA-pipe ops each);
-  // k minimises max(MUFU work / 16, FMA work / 128) per evaluation (RK4 combination included).
-  std::set<int> emul;
-  if (balance) {
-    SignSelect probe(g, live, roots);
+  // moves work to the FMA pipe: (1) sigmoids in pairs share one reciprocal (1/dA = dB/(dA dB): one
+  // MUFU.RCP instead of two, for 3 FMA-pipe ops), (2) K of the exponentials of a particle-step (4 RHS
+  // evaluations) run as ff_exp2p (8 FMA-pipe ops each). K is split over the 4 RK4 stages (k or k + 1
+  // per stage: two emitted RHS variants), so the balance is set per particle-step, not per
+  // evaluation. Chosen to minimise max(MUFU / 16, FMA / 128) per particle-step (RK4 combination in).
+  std::vector<int> cand;   // exponentials (exp / sigmoid nodes), in creation order
+  std::vector<int> sigs;   // sigmoid nodes
+  for (size_t id = 0; id < g.nodes.size(); ++id)
+    if (live[id] && !g.nodes[id].uniform && (g.nodes[id].k == K::Exp2 || g.nodes[id].k == K::Sigmoid2)) {
+      cand.push_back((int)id);
+      if (g.nodes[id].k == K::Sigmoid2) sigs.push_back((int)id);
+    }
+  std::map<int, int> pairs;
+  for (size_t i = 0; i + 1 < sigs.size(); i += 2) {
+    pairs[sigs[i]] = sigs[i + 1];
+    pairs[sigs[i + 1]] = sigs[i];
+  }
+  auto probe_counts = [&](const std::map<int, int>& pr, double& a, double& m) {
+    SignSelect probe(g, live, roots, {}, pr);
     for (int i = 0; i < s.dim; ++i) {
       const int r = roots[i];
       probe.get(r, (!g.nodes[r].uniform && probe.cost(r, 1) < probe.cost(r, 0)) ? 1 : 0);
     }
-    std::vector<int> cand;
-    for (size_t id = 0; id < g.nodes.size(); ++id)
-      if (live[id] && !g.nodes[id].uniform && (g.nodes[id].k == K::Exp2 || g.nodes[id].k == K::Sigmoid2))
-        cand.push_back((int)id);
-    const double a = probe.n_arith + 7.0 * s.dim / 4.0, m = probe.n_mufu;
-    int best_k = 0;
-    double best_t = std::max(m / 16.0, a / 128.0);
-    for (int k = 1; k <= (int)cand.size(); ++k) {
-      const double t = std::max((m - k) / 16.0, (a + SignSelect::kExp2pOps * k) / 128.0);
-      if (t < best_t - 1e-9) { best_t = t; best_k = k; }
+    a = probe.n_arith;
+    m = probe.n_mufu;
+  };
+  bool use_pairs = false;
+  int K = 0;   // exponentials per particle-step on the FMA pipe
+  // selection cost of one ff_exp2p: its 8 FMA-pipe ops plus ~4 issue slots of ALU work (clamp,
+  // exponent assembly); measured on B200 (STN-GPe bifurcation, sigmoid pairs on): K = 0, 1, 2, 3 per
+  // particle-step -> 3.56, 3.64, 3.35, 3.07e11 particle-steps/s, which a cost of 8 would mis-rank
+  constexpr double kExp2pCost = 12.0;
+  if (balance) {
+    double best_t = 1e30;
+    for (int pv = 0; pv < (pairs.empty() ? 1 : 2); ++pv) {
+      double a, m;
+      probe_counts(pv ? pairs : std::map<int, int>{}, a, m);
+      const double A = 4 * a + 7.0 * s.dim, M = 4 * m;
+      for (int k = 0; k <= 4 * (int)cand.size(); ++k) {
+        const double t = std::max((M - k) / 16.0, (A + kExp2pCost * k) / 128.0);
+        if (t < best_t - 1e-9) { best_t = t; K = k; use_pairs = pv != 0; }
+      }
     }
-    if (const char* e = std::getenv("FF_TUNE_EXP2P")) best_k = std::min((int)cand.size(), std::max(0, std::atoi(e)));
-    for (int k = 0; k < best_k; ++k) emul.insert(cand[k]);
+    if (const char* e = std::getenv("FF_TUNE_EXP2P"))   // exponentials per evaluation, every stage
+      K = 4 * std::min((int)cand.size(), std::max(0, std::atoi(e)));
+    if (const char* e = std::getenv("FF_TUNE_EXP2P_STEP"))   // exponentials per particle-step
+      K = std::min(4 * (int)cand.size(), std::max(0, std::atoi(e)));
+    if (const char* e = std::getenv("FF_TUNE_RCP_PAIRS")) use_pairs = std::atoi(e) != 0 && !pairs.empty();
   }
-  SignSelect sel(g, live, roots, emul);
+  const int k_lo = K / 4, n_hi = K % 4;   // stages 0 .. n_hi-1 run k_lo + 1 on the FMA pipe
+  auto emul_set = [&](int k) {
+    std::set<int> e;
+    for (int i = 0; i < k && i < (int)cand.size(); ++i) e.insert(cand[i]);
+    return e;
+  };
+  QTable qtab;
+  const std::map<int, int> used_pairs = use_pairs ? pairs : std::map<int, int>{};
+  SignSelect sel(g, live, roots, emul_set(k_lo), used_pairs, &qtab);
   std::vector<int> sign(s.dim, 1);
   std::vector<std::string> out(s.dim);
   for (int i = 0; i < s.dim; ++i) {
@@ -1178,7 +1251,14 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
     if (!g.nodes[r].uniform && sel.cost(r, 1) < sel.cost(r, 0)) sign[i] = -1;
     out[i] = sel.get(r, sign[i] < 0 ? 1 : 0);
   }
-  const int n_arith = sel.n_arith, n_mufu = sel.n_mufu;
+  // the second variant (one more exponential on the FMA pipe), same signs and q table
+  SignSelect sel_hi(g, live, roots, emul_set(k_lo + 1), used_pairs, &qtab);
+  std::vector<std::string> out_hi(s.dim);
+  if (n_hi)
+    for (int i = 0; i < s.dim; ++i) out_hi[i] = sel_hi.get(roots[i], sign[i] < 0 ? 1 : 0);
+  // per particle-step (4 evaluations)
+  const int n_arith = (4 - n_hi) * sel.n_arith + n_hi * sel_hi.n_arith;
+  const int n_mufu = (4 - n_hi) * sel.n_mufu + n_hi * sel_hi.n_mufu;
   if (prog) {  // the q values as a host program: every uniform node they reach, in creation order
     prog->ops.clear();
     prog->q.clear();
@@ -1192,7 +1272,7 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
       prog->ops.push_back(o);
       return at[id] = (int)prog->ops.size() - 1;
     };
-    for (const auto& e : sel.qlist) prog->q.push_back({put(e.first), e.second});
+    for (const auto& e : qtab.list) prog->q.push_back({put(e.first), e.second});
   }
   std::ostringstream rhs;
   rhs << "// Generated right-hand side (" << s.dim << " state variables, " << s.param_names.size()
@@ -1201,22 +1281,38 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   for (size_t k = 0; k < s.param_names.size(); ++k)
     rhs << "//   a.p[" << k << "] = " << s.param_names[k]
         << ((int)k == sweep_param ? "  (swept: the per-particle value sw is used instead)" : "") << "\n";
-  rhs << "// per evaluation (front-end count): " << n_arith << " arithmetic ops, " << n_mufu << " MUFU ops\n";
-  rhs << "// exponentials on the FMA pipe (pipe balancing): " << emul.size() << "\n";
+  rhs << "// per particle-step, 4 evaluations (front-end count): " << n_arith << " arithmetic ops, " << n_mufu
+      << " MUFU ops\n";
+  rhs << "// exponentials on the FMA pipe per particle-step (pipe balancing): " << K
+      << "; sigmoid pairs sharing a reciprocal: " << (use_pairs ? (int)pairs.size() / 2 : 0) << "\n";
   rhs << "// plain formulation (no gating rewrite, uniform factors multiplied in every evaluation): "
-      << n_arith_plain << " arithmetic ops, " << n_mufu_plain << " MUFU ops, " << n_exp_plain << " exponentials\n";
-  rhs << "template <class V>\n__device__ __forceinline__ void ff_rhs(const V* __restrict__ x, V* __restrict__ dx, "
-         "const FFStepArgs& a, const V& sw) {\n";
-  rhs << "  (void)a; (void)sw;\n";
-  rhs << "  const V nsw = -sw; (void)nsw;\n";
-  rhs << sel.body.str();
-  for (int i = 0; i < s.dim; ++i) {
-    const DNode& r = g.nodes[roots[i]];
-    rhs << "  dx[" << i << "] = " << (r.uniform ? "ff_bcast<V>(" + out[i] + ")" : out[i]) << ";"
-        << (sign[i] < 0 || slot[i] >= 0 ? "  // = d" + s.var_names[i] + "/dt" + (sign[i] < 0 ? " * (-1)" : "") +
-                                              (slot[i] >= 0 ? " / scale" : "") : "")
-        << "\n";
-  }
+      << n_arith_plain << " arithmetic ops, " << n_mufu_plain << " MUFU ops, " << n_exp_plain << " exponentials, "
+      << n_sig_plain / 2 << " sigmoid pairs\n";
+  auto emit_rhs = [&](const std::string& fname, SignSelect& ss, const std::vector<std::string>& o) {
+    rhs << "template <class V>\n__device__ __forceinline__ void " << fname
+        << "(const V* __restrict__ x, V* __restrict__ dx, const FFStepArgs& a, const V& sw) {\n";
+    rhs << "  (void)a; (void)sw;\n";
+    rhs << "  const V nsw = -sw; (void)nsw;\n";
+    rhs << ss.body.str();
+    for (int i = 0; i < s.dim; ++i) {
+      const DNode& r = g.nodes[roots[i]];
+      rhs << "  dx[" << i << "] = " << (r.uniform ? "ff_bcast<V>(" + o[i] + ")" : o[i]) << ";"
+          << (sign[i] < 0 || slot[i] >= 0 ? "  // = d" + s.var_names[i] + "/dt" + (sign[i] < 0 ? " * (-1)" : "") +
+                                                (slot[i] >= 0 ? " / scale" : "") : "")
+          << "\n";
+    }
+    rhs << "}\n";
+  };
+  emit_rhs("ff_rhs_v0", sel, out);
+  if (n_hi) emit_rhs("ff_rhs_v1", sel_hi, out_hi);
+  // RK4 stage s evaluates variant FF_STAGE_VAR[s] (pipe balancing per particle-step)
+  rhs << "__device__ constexpr int FF_STAGE_VAR[4] = {";
+  for (int st = 0; st < 4; ++st) rhs << (st ? ", " : "") << (st < n_hi ? 1 : 0);
+  rhs << "};\n";
+  rhs << "template <int STAGE, class V>\n__device__ __forceinline__ void ff_rhs(const V* __restrict__ x, "
+         "V* __restrict__ dx, const FFStepArgs& a, const V& sw) {\n";
+  if (n_hi) rhs << "  if (FF_STAGE_VAR[STAGE]) ff_rhs_v1<V>(x, dx, a, sw); else ff_rhs_v0<V>(x, dx, a, sw);\n";
+  else rhs << "  ff_rhs_v0<V>(x, dx, a, sw);\n";
   rhs << "}\n";
   rhs << "// dx[d] holds FF_SIGN[d] * f_d(x) / scale_d: a component computed negated saves FFMA2\n"
          "// negations, a uniform factor scale_d (slot FF_SSLOT[d] >= 0) saves a multiply; the integrator\n"

@@ -53,8 +53,8 @@ def test_emit_contains_equations_and_sweep_variant():
     s = systems.lorenz()
     src = FF.ff_emit_source(s, sweep_param=1)
     assert "(swept: the per-particle value sw is used instead)" in src
-    assert "sw" in src[src.index("void ff_rhs(const V* __restrict__"):]
-    assert "a.p[1]" not in src[src.index("void ff_rhs(const V* __restrict__"):src.index("per-slot helpers")]
+    assert "sw" in src[src.index("void ff_rhs_v0(const V* __restrict__"):]
+    assert "a.p[1]" not in src[src.index("void ff_rhs_v0(const V* __restrict__"):src.index("per-slot helpers")]
 
 
 def test_nvrtc_compiles_sm100a_cubin():
@@ -107,11 +107,11 @@ def test_validation_errors():
 def test_precedence_and_folding():
     # "-x^2" is -(x^2); integer powers expand to products; exp folds log2(e)
     src = FF.ff_emit_source(systems.SystemDef("t", ["x"], ["-x^2 + exp(-x/2)"], []))
-    body = src[src.index("void ff_rhs(const V* __restrict__"):src.index("per-slot helpers")]
+    body = src[src.index("void ff_rhs_v0(const V* __restrict__"):src.index("per-slot helpers")]
     assert "x[0] * x[0]" in body
     assert "-0.721347511f * x[0]" in body and "ff_exp2(t" in body
     src = FF.ff_emit_source(systems.SystemDef("t", ["x"], ["2^3 + x*0 + 2*(3 - x)"], []))
-    body = src[src.index("void ff_rhs(const V* __restrict__"):src.index("per-slot helpers")]
+    body = src[src.index("void ff_rhs_v0(const V* __restrict__"):src.index("per-slot helpers")]
     assert "8.0f" in body and "6.0f" in body
 
 

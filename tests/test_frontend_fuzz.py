@@ -17,7 +17,7 @@ def test_random_systems_emit(seed):
     s = SystemDef("fuzz", vars_, texts, [(p, v, None, None) for p, v in pvals.items()])
     a = FF.ff_emit_source(s)
     assert a == FF.ff_emit_source(s)
-    body = a[a.index("void ff_rhs(const V* __restrict__"):]
+    body = a[a.index("void ff_rhs_v0(const V* __restrict__"):]
     body = body[:body.index("\n}\n")]
     assert not re.search(r"(^|\W)(if|for|while|switch|goto)(\W|$)", body.split("\n", 1)[1])
     for i in range(len(vars_)):
@@ -66,7 +66,7 @@ def test_structured_systems_emit_with_rewrites(seed):
     assert a == FF.ff_emit_source(s)
     slots = [int(v) for v in re.search(r"FF_SSLOT\[FF_DIM\] = \{([^}]*)\}", a).group(1).split(",")]
     assert max(slots) >= 0 and max(slots) < 4
-    body = a[a.index("void ff_rhs(const V* __restrict__"):]
+    body = a[a.index("void ff_rhs_v0(const V* __restrict__"):]
     body = body[:body.index("\n}\n")]
     assert not re.search(r"(^|\W)(if|for|while|switch|goto)(\W|$)", body.split("\n", 1)[1])
 

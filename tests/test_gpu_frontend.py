@@ -41,7 +41,7 @@ def test_exponentials_on_the_fma_pipe(monkeypatch, ppt, tpb):
     monkeypatch.setenv("FF_TUNE_EXP2P", "99")
     n, lo, hi = 9000 + 5, [-2.0, -2.0, -1.5], [2.0, 2.0, 1.5]
     src = FF.ff_emit_source(FUNCS)
-    assert "ff_exp2p(" in src and "exponentials on the FMA pipe (pipe balancing): 2" in src
+    assert "ff_exp2p(" in src and "exponentials on the FMA pipe per particle-step (pipe balancing): 8" in src
     ctx = FF.Context(FUNCS, [n])
     ctx.set_launch(ppt, tpb)
     g = ctx.init_group(lo, hi, n, 1, 0, seed=31)
