@@ -334,7 +334,6 @@ std::vector<int> split_scales(const System& s, int sweep_param, std::vector<Node
   // components with the same factor share a slot (HH ring: dV_i/dt = (...)/C for every neuron), so
   // the kernel keeps fewer loop-invariant step constants in uniform registers
   std::map<std::string, int> seen;
-  std::vector<NodeP> first;
   for (int d = 0; d < s.dim; ++d) {
     std::vector<NodeP> uni, var;
     factors(s.rhs[d], sweep_param, uni, var);

@@ -57,8 +57,9 @@ System parse_system(const ff_system* sys);
 // f_d = scale_d * rest_d with scale_d a product of factors that depend on parameters only (not on
 // state variables, not on the swept parameter `sweep_param`). The kernel integrates rest_d with step
 // constants h * scale_d computed by the host per launch, so the RHS never multiplies by scale_d.
-// At most FF_MAX_SCALED components are split (the first ones); returns the slot of every component
-// (-1 = not split) and fills rest (every component) and scale (every split one, else null).
+// Components with the same factor share a slot; at most FF_MAX_SCALED distinct factors (the first
+// ones). Returns the slot of every component (-1 = not split) and fills rest (every component) and
+// scale (every split one, else null).
 std::vector<int> split_scales(const System& s, int sweep_param, std::vector<NodeP>* rest,
                               std::vector<NodeP>* scale);
 // Value (double) of a parameter-only expression for the given parameter values.
