@@ -11,8 +11,8 @@ from paper_1505_00344_b200 import systems
 def timeit(n_half, S, reps=10):
     ctx = FF.Context(systems.lorenz(), [n_half, n_half])
     ctx.init_group([-10, -30, 0], [10, 30, 50], n_half, 1, 0, 2)
-    ctx.init_group([-10, -30, 0], [10, 30, 50], n_half, -1, 1, 3)
-    ctx.set_reset(True)                     # keep backward particles finite
+    ctx.init_group([-10, -30, 0], [10, 30, 50], n_half, 1, 1, 3)
+    ctx.set_param("r", 0.5)                 # bounded trajectories, no reset bookkeeping
     ts = []
     for i in range(reps + 2):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
