@@ -70,7 +70,7 @@ struct FFStepArgs {
   // lo_k) * s_k, 0, 1))) of its projected axis values, summed per pixel into colour_img[3][H][W]
   ff_u32* colour_img;   // null = off
   float col_lo[3], col_s[3];
-  int pad2_;
+  int static_rounds;    // tile rounds assigned statically (block b: b, b + grid, ...) before the counter
   float bound_lo[FF_MAX_DIM_], bound_hi[FF_MAX_DIM_];
   FFGroup g[FF_MAX_GROUPS_];
   // step constants of the components with a factored uniform scale s (FF_SSLOT[d] in the generated

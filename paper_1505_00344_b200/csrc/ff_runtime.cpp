@@ -378,9 +378,14 @@ struct ff_ctx {
     int64_t resident = (int64_t)nsm * occ;
     if (grid_limit > 0 && grid_limit < resident) resident = grid_limit;
     const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
+    // static tile rounds for 1-2-step launches (ff_step_body): all but the last round of tiles
+    const int64_t ns = (n_steps <= 2 && sys.dim <= 8 && ntiles / grid >= 2) ? ntiles / grid - 1 : 0;
+    a.static_rounds = (int)ns;
     void* args[] = {&a};
     ck(cudaLaunchKernel((const void*)kern, dim3(grid), dim3(t), args, dyn_smem, stream), "launch ff_step");
-    tile_base += (uint64_t)ntiles + grid;  // each block fetches until it sees a tile >= ntiles
+    // static rounds first (ff_step_body), then each block fetches dynamic tiles until it sees one past
+    // the end: the counter advances by the dynamic tiles + grid
+    tile_base += (uint64_t)(ntiles - ns * (int64_t)grid) + grid;
     ++launches;
     if (xworld > 1 && image) launch_exchange(m);  // (one rank: its image already is the sum)
   }

@@ -1,0 +1,4 @@
+# Static tile rounds + dynamic remainder: GPU suite + benches + fixed-cost decomposition.
+timeout 1500 python -m pytest tests -m gpu -q -x -rf > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
+for v in "" "--S 10" "--S 1" "--S 1000" "--S 1 --no-image" "--config hh" "--config stn_bif3d" "--config sweep" "--config stn" "--config lorenz3d_collapsed"; do timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e $v 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', '%.4g'%d['value'], '%.3f'%d['roofline']['frac'], '%.1f us'%(1000*d['kernel_ms_mean']))"; done
+PYTHONPATH=$PWD python tools/fixedcost.py
