@@ -485,3 +485,24 @@ def test_async_state_and_image_copies():
     assert np.array_equal(ctx.read_state(g), src.numpy())
     assert np.array_equal(out.numpy().view(np.uint32), ctx.read_image())
     assert np.array_equal(ctx.read_image(), O.histogram(src.numpy(), [0, 2], [-20.0, 20.0, 0.0, 50.0], 64, 48, 1, 0))
+
+
+@pytest.mark.parametrize("W,H,fov,eye,axes", [
+    (1280, 720, 60.0, (80.0, -90.0, 60.0), [0, 1, 2]),      # wide image, oblique camera
+    (333, 517, 30.0, (0.0, 10.0, 140.0), [2, 0, 1]),        # odd sizes, permuted axes, looking down
+])
+def test_histogram_3d_other_cameras_bit_exact(W, H, fov, eye, axes):
+    """3-D binning with non-square / odd images, other view-projection matrices and permuted axes
+    (reading R17-R18), bit-exact vs the oracle on identical coordinates."""
+    rng = np.random.default_rng(53)
+    n = 30000 + 7
+    ctx = lorenz_ctx([n])
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=1)
+    x = np.stack([rng.uniform(-40, 40, n), rng.uniform(-60, 60, n), rng.uniform(-10, 80, n)]).astype(np.float32)
+    ctx.write_state(g, x)
+    Mv = views.look_at(eye, (0.0, 0.0, 25.0), (0.0, 0.0, 1.0) if eye[2] < 100 else (0.0, 1.0, 0.0))
+    M = (views.perspective(fov, W / H, 1.0, 1000.0) @ Mv).astype(np.float32)
+    ctx.project(axes, M, W, H, 1)
+    want = O.histogram(x, axes, M, W, H, 1, 0)
+    assert want.sum() > n // 4
+    assert np.array_equal(ctx.read_image(), want)
