@@ -530,3 +530,52 @@ def test_swept_shards_sum_to_whole(mode):
     parts = [run(r, 3) for r in range(3)]
     assert np.array_equal(sum(p[0] for p in parts), whole) and whole.sum() > 0
     assert np.array_equal(np.hstack([p[1] for p in parts]).view(np.uint32), sw.view(np.uint32))
+
+
+def test_stn_bifurcation_throughput_variant_sampled():
+    """STN-GPe with w_ss swept over [0, 12) (NEXT 4) at a size that selects the
+    pipe-balanced throughput kernel (both sigmoids of an evaluation share one reciprocal, one
+    exponential per particle-step on the FMA pipe): sampled slices of both groups, including the ragged tail,
+    against the oracle at Tier A after 100 steps."""
+    p, s = stn_params()
+    n = 50000 + 19
+    ctx = FF.Context(s, [n, n])
+    gs = [ctx.init_group([0, 0], [1, 1], n, d, 0, seed=31 + k) for k, d in enumerate((1, -1))]
+    for g in gs:
+        ctx.sweep_param(g, "w_ss", 0.0, 12.0, 0, 23)
+    ctx.step(100, 0.01)
+    for k, (g, h) in enumerate(zip(gs, (0.01, -0.01))):
+        got = ctx.read_state(g)
+        for first, count in ((0, 1500), (24000, 1500), (n - 1501, 1501)):
+            sv = O.sweep_values(0.0, 12.0, 0, 23, first, count, n)
+            want = oracle_group(O.STN, [0, 0], [1, 1], 31 + k, first, count, p, h, 100, 0, sv)
+            assert tier_a(got[:, first:first + count], want, [1.0, 1.0]) <= 1e-5
+
+
+def test_stn_poisoned_neighbours_do_not_leak():
+    """Particles stay independent in the throughput kernel (two particles per thread in packed
+    FFMA2 pairs, clamped sigmoid-pair denominators): with a third of the states replaced by NaN, +-inf
+    or +-1e30, every other particle ends bit-identical to the unpoisoned run -- no value, and no
+    rounding, crosses between the lanes of a pair (the rejected lane-shared reciprocal)."""
+    _, s = stn_params()
+    n = 100000 + 3
+    rng = np.random.default_rng(60)
+
+    def run(x):
+        ctx = FF.Context(s, [n])
+        g = ctx.init_group([0, 0], [1, 1], n, 1, 0, seed=41)
+        ctx.sweep_param(g, "w_ss", 0.0, 12.0, 0, 23)
+        if x is not None:
+            ctx.write_state(g, x)
+        x0 = ctx.read_state(g)
+        ctx.step(50, 0.01)
+        return x0, ctx.read_state(g)
+
+    x0, clean = run(None)
+    bad = rng.random(n) < 1 / 3
+    poison = np.array([np.nan, np.inf, -np.inf, 1e30, -1e30], np.float32)
+    xp = x0.copy()
+    xp[:, bad] = poison[rng.integers(0, len(poison), (2, int(bad.sum())))]
+    _, dirty = run(xp)
+    assert np.isfinite(clean).all()
+    assert np.array_equal(dirty[:, ~bad].view(np.uint32), clean[:, ~bad].view(np.uint32))
