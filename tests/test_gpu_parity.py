@@ -552,30 +552,44 @@ def test_stn_bifurcation_throughput_variant_sampled():
             assert tier_a(got[:, first:first + count], want, [1.0, 1.0]) <= 1e-5
 
 
-def test_stn_poisoned_neighbours_do_not_leak():
+POISON_CASES = [
+    ("stn_bif3d", lambda: systems.stn_gpe(), [0.0, 0.0], [1.0, 1.0], ("w_ss", 0.0, 12.0), [0, 1]),
+    ("lorenz_r_swept", lambda: systems.lorenz(), LZ_LO, LZ_HI, ("r", 0.0, 200.0), [0, 2]),
+    ("hh_ring3", lambda: systems.hh_ring(3), HH_LO, HH_HI, None, [0, 5]),
+]
+
+
+@pytest.mark.parametrize("name,make,lo,hi,sweep,axes", POISON_CASES, ids=[c[0] for c in POISON_CASES])
+def test_poisoned_neighbours_do_not_leak(name, make, lo, hi, sweep, axes):
     """Particles stay independent in the throughput kernel (two particles per thread in packed
-    FFMA2 pairs, clamped sigmoid-pair denominators): with a third of the states replaced by NaN, +-inf
-    or +-1e30, every other particle ends bit-identical to the unpoisoned run -- no value, and no
-    rounding, crosses between the lanes of a pair (the rejected lane-shared reciprocal)."""
-    _, s = stn_params()
+    FFMA2 pairs; STN-GPe: clamped sigmoid-pair denominators): with a third of the states replaced by
+    NaN, +-inf or +-1e30, every other particle ends bit-identical to the unpoisoned run -- no value,
+    and no rounding, crosses between the lanes of a pair (the rejected lane-shared
+    reciprocal) -- and the fused binning counts exactly the finite in-window particles."""
+    s = make()
     n = 100000 + 3
     rng = np.random.default_rng(60)
+    view = [float(lo[axes[0]]), float(hi[axes[0]]), float(lo[axes[1]]), float(hi[axes[1]])]
 
     def run(x):
         ctx = FF.Context(s, [n])
-        g = ctx.init_group([0, 0], [1, 1], n, 1, 0, seed=41)
-        ctx.sweep_param(g, "w_ss", 0.0, 12.0, 0, 23)
+        g = ctx.init_group(lo, hi, n, 1, 0, seed=41)
+        if sweep:
+            ctx.sweep_param(g, sweep[0], sweep[1], sweep[2], 0, 23)
         if x is not None:
             ctx.write_state(g, x)
         x0 = ctx.read_state(g)
-        ctx.step(50, 0.01)
-        return x0, ctx.read_state(g)
+        ctx.project(axes, view, 256, 256, 1).zero_()
+        ctx.step(20, 0.01)
+        return x0, ctx.read_state(g), ctx.read_image()
 
-    x0, clean = run(None)
+    x0, clean, _ = run(None)
     bad = rng.random(n) < 1 / 3
     poison = np.array([np.nan, np.inf, -np.inf, 1e30, -1e30], np.float32)
     xp = x0.copy()
-    xp[:, bad] = poison[rng.integers(0, len(poison), (2, int(bad.sum())))]
-    _, dirty = run(xp)
+    xp[:, bad] = poison[rng.integers(0, len(poison), (xp.shape[0], int(bad.sum())))]
+    _, dirty, img = run(xp)
     assert np.isfinite(clean).all()
     assert np.array_equal(dirty[:, ~bad].view(np.uint32), clean[:, ~bad].view(np.uint32))
+    want = O.histogram(dirty, axes, view, 256, 256, 1, 0)
+    assert np.array_equal(img, want)
