@@ -339,6 +339,7 @@ def run_ours(args, w, rank, world, device):
 
 EXP2P_OPS = 8   # FMA-pipe ops of one exponential computed on the FMA pipe (ff_exp2p in ff_device.cuh)
 PAIR_OPS = 3    # FMA-pipe ops that let two sigmoids share one reciprocal (one MUFU.RCP fewer)
+RCPP_OPS = 7    # FMA-pipe ops of a pair reciprocal computed on the FMA pipe (ff_rcpp in ff_device.cuh)
 
 
 def op_counts(sysdef, sweep_idx):
@@ -363,16 +364,19 @@ def op_counts(sysdef, sweep_idx):
 def balanced_work(fma_ops, mufu_ops, n_exp, n_pairs=0):
     """FP32-pipe-equivalent work per particle-step of the pipe-balanced roofline: the FMA and MUFU
     pipes run concurrently (128 and 16 results / clk / SM); any exponential can move from MUFU to the
-    FMA pipe at EXP2P_OPS ops, and two sigmoids can share one reciprocal for PAIR_OPS ops, so the
-    least time per particle-step on one SM is T = min over k, pairing of
-    max((mufu - pairs - k) / 16, (fma + PAIR_OPS pairs + EXP2P_OPS k) / 128) cycles; work = 128 T
-    lane-ops (= fma for an FMA-bound system). Returns (work, k, binding pipes)."""
+    FMA pipe at EXP2P_OPS ops, two sigmoids can share one reciprocal for PAIR_OPS ops, and r of those
+    shared reciprocals can run on the FMA pipe at RCPP_OPS ops, so the least time per particle-step on
+    one SM is T = min over k, pairing, r of max((mufu - pairs - k - r) / 16,
+    (fma + PAIR_OPS pairs + EXP2P_OPS k + RCPP_OPS r) / 128) cycles; work = 128 T lane-ops (= fma
+    for an FMA-bound system). Returns (work, k, binding pipes)."""
     best = (max(mufu_ops / XU_LANES, fma_ops / FMA_LANES), 0, 0)
     for pr in ((0, n_pairs) if n_pairs else (0,)):
         for k in range(0, n_exp + 1):
-            t = max((mufu_ops - pr - k) / XU_LANES, (fma_ops + PAIR_OPS * pr + EXP2P_OPS * k) / FMA_LANES)
-            if t < best[0] - 1e-12:
-                best = (t, k, pr)
+            for r in range(0, pr + 1):
+                t = max((mufu_ops - pr - k - r) / XU_LANES,
+                        (fma_ops + PAIR_OPS * pr + EXP2P_OPS * k + RCPP_OPS * r) / FMA_LANES)
+                if t < best[0] - 1e-12:
+                    best = (t, k, pr or r)
     t, k, pr = best
     moved = k or pr
     pipes = "fma" if fma_ops / FMA_LANES >= mufu_ops / XU_LANES and not moved else ("xu" if not moved else "fma+xu")

@@ -840,6 +840,10 @@ struct SignSelect {
   // sigmoid pairs sharing one reciprocal: 1/dA = dB / (dA dB), 1/dB = dA / (dA dB) (pipe balancing)
   std::map<int, int> pair_of;
   static constexpr int kPairOps = 3;   // dA dB, dB P, dA P (the clamps run on the ALU pipe)
+  // the pairs' reciprocals on the FMA pipe (ff_rcpp: 6 FMA-pipe ops and the negation of the
+  // denominator, which packed FFMA2 cannot fold into an operand; + 1 integer op)
+  bool rcpp = false;
+  static constexpr int kRcppOps = 7;
   QTable own_q;
   QTable* qt;
   SignSelect(const Dag& dag, const std::vector<char>& lv, const std::vector<int>& roots, std::set<int> em = {},
@@ -972,11 +976,11 @@ struct SignSelect {
     // exponentials clamped at 2^60 so the product stays finite (a sigmoid below 1e-18 is 0 here)
     body << "  const V " << da << " = 1.0f + ff_min(" << ea << ", 1.15292150e18f);\n";
     body << "  const V " << db << " = 1.0f + ff_min(" << eb << ", 1.15292150e18f);\n";
-    body << "  const V " << pr << " = ff_rcp(" << da << " * " << db << ");\n";
+    body << "  const V " << pr << " = " << (rcpp ? "ff_rcpp(" : "ff_rcp(") << da << " * " << db << ");\n";
     body << "  const V " << sa << " = " << db << " * " << pr << ";\n";
     body << "  const V " << sb << " = " << da << " * " << pr << ";\n";
-    n_arith += 2 + kPairOps;
-    ++n_mufu;
+    n_arith += 2 + kPairOps + (rcpp ? kRcppOps : 0);
+    n_mufu += rcpp ? 0 : 1;
     memo[{a, 0}] = sa;
     memo[{b, 0}] = sb;
     return memo[{id, 0}];
@@ -1217,24 +1221,49 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   // exponent assembly); measured on B200 (STN-GPe bifurcation, sigmoid pairs on): K = 0, 1, 2, 3 per
   // particle-step -> 3.56, 3.64, 3.35, 3.07e11 particle-steps/s, which a cost of 8 would mis-rank
   constexpr double kExp2pCost = 12.0;
+  // the same for a pair reciprocal on the FMA pipe (ff_rcpp, 7 ops): measured on the STN-GPe
+  // bifurcation with pairs and no exponential moved, R = 0..4 stages -> 3.58, 3.70, 3.44, 3.18,
+  // 2.98e11 (tools/gpu_run62.sh), which a cost of 12 ranks; ties go to fewer executed ops
+  constexpr double kRcppCost = 12.0;
+  int R = 0;   // stages (of 4) whose pair reciprocals run on the FMA pipe (with k_lo exponentials)
+  const int n_pair_eval = (int)pairs.size() / 2;
   if (balance) {
-    double best_t = 1e30;
+    double best_t = 1e30, best_ops = 1e30;
+    auto take = [&](double t, double ops, int k, int r, bool pv) {
+      if (t < best_t - 1e-9 || (t < best_t + 1e-9 && ops < best_ops - 1e-9)) {
+        best_t = t; best_ops = ops; K = k; R = r; use_pairs = pv;
+      }
+    };
     for (int pv = 0; pv < (pairs.empty() ? 1 : 2); ++pv) {
       double a, m;
       probe_counts(pv ? pairs : std::map<int, int>{}, a, m);
       const double A = 4 * a + 7.0 * s.dim, M = 4 * m;
-      for (int k = 0; k <= 4 * (int)cand.size(); ++k) {
-        const double t = std::max((M - k) / 16.0, (A + kExp2pCost * k) / 128.0);
-        if (t < best_t - 1e-9) { best_t = t; K = k; use_pairs = pv != 0; }
-      }
+      for (int k = 0; k <= 4 * (int)cand.size(); ++k)
+        take(std::max((M - k) / 16.0, (A + kExp2pCost * k) / 128.0), A + SignSelect::kExp2pOps * k, k, 0, pv);
+      if (pv)   // k_lo exponentials in every stage, the pair reciprocals of r stages on the FMA pipe
+        for (int k = 0; k <= (int)cand.size(); ++k)
+          for (int r = 1; r <= 4; ++r) {
+            const double mr = M - 4 * k - r * n_pair_eval;
+            const double t = std::max(mr / 16.0, (A + kExp2pCost * 4 * k + kRcppCost * r * n_pair_eval) / 128.0);
+            take(t, A + SignSelect::kExp2pOps * 4 * k + SignSelect::kRcppOps * r * n_pair_eval, 4 * k, r, true);
+          }
     }
     if (const char* e = std::getenv("FF_TUNE_EXP2P"))   // exponentials per evaluation, every stage
       K = 4 * std::min((int)cand.size(), std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("FF_TUNE_EXP2P_STEP"))   // exponentials per particle-step
       K = std::min(4 * (int)cand.size(), std::max(0, std::atoi(e)));
+    if (std::getenv("FF_TUNE_EXP2P") || std::getenv("FF_TUNE_EXP2P_STEP")) R = 0;
+    if (const char* e = std::getenv("FF_TUNE_RCPP_STAGES")) {   // (K then rounds down to 4 k_lo)
+      R = std::min(4, std::max(0, std::atoi(e)));
+      if (R) K -= K % 4;
+    }
     if (const char* e = std::getenv("FF_TUNE_RCP_PAIRS")) use_pairs = std::atoi(e) != 0 && !pairs.empty();
+    if (!use_pairs) R = 0;
   }
-  const int k_lo = K / 4, n_hi = K % 4;   // stages 0 .. n_hi-1 run k_lo + 1 on the FMA pipe
+  // stages 0 .. n_hi-1 run variant 1: k_lo + 1 exponentials on the FMA pipe, or (R > 0) k_lo and
+  // their pair reciprocals on the FMA pipe
+  const bool hi_rcpp = R > 0;
+  const int k_lo = K / 4, n_hi = hi_rcpp ? R : K % 4;
   auto emul_set = [&](int k) {
     std::set<int> e;
     for (int i = 0; i < k && i < (int)cand.size(); ++i) e.insert(cand[i]);
@@ -1251,7 +1280,8 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
     out[i] = sel.get(r, sign[i] < 0 ? 1 : 0);
   }
   // the second variant (one more exponential on the FMA pipe), same signs and q table
-  SignSelect sel_hi(g, live, roots, emul_set(k_lo + 1), used_pairs, &qtab);
+  SignSelect sel_hi(g, live, roots, emul_set(hi_rcpp ? k_lo : k_lo + 1), used_pairs, &qtab);
+  sel_hi.rcpp = hi_rcpp;
   std::vector<std::string> out_hi(s.dim);
   if (n_hi)
     for (int i = 0; i < s.dim; ++i) out_hi[i] = sel_hi.get(roots[i], sign[i] < 0 ? 1 : 0);
@@ -1283,7 +1313,8 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   rhs << "// per particle-step, 4 evaluations (front-end count): " << n_arith << " arithmetic ops, " << n_mufu
       << " MUFU ops\n";
   rhs << "// exponentials on the FMA pipe per particle-step (pipe balancing): " << K
-      << "; sigmoid pairs sharing a reciprocal: " << (use_pairs ? (int)pairs.size() / 2 : 0) << "\n";
+      << "; sigmoid pairs sharing a reciprocal: " << (use_pairs ? (int)pairs.size() / 2 : 0)
+      << "; stages with the pair reciprocals on the FMA pipe: " << R << "\n";
   rhs << "// plain formulation (no gating rewrite, uniform factors multiplied in every evaluation): "
       << n_arith_plain << " arithmetic ops, " << n_mufu_plain << " MUFU ops, " << n_exp_plain << " exponentials, "
       << n_sig_plain / 2 << " sigmoid pairs\n";

@@ -71,3 +71,34 @@ def test_exp2p_extreme_arguments():
     assert np.all(got[0][x0[0] > 90] > x0[0][x0[0] > 90])          # huge positive (or +inf)
     s = (got[1] - x0[1]).astype(np.float64) / 1e-3
     assert np.all(np.abs(s[x0[1] > 100] - 1) < 0.1) and np.all(np.abs(s[x0[1] < -100]) < 0.1)   # ulp(400) = 3e-5
+
+
+@pytest.mark.parametrize("stages", ["0", "4"])
+def test_pair_reciprocals_on_the_fma_pipe(monkeypatch, stages):
+    """Pipe balancing: the two sigmoids of an evaluation share one reciprocal (exponentials clamped at
+    2^60), and with FF_TUNE_RCPP_STAGES=4 that reciprocal runs on the FMA pipe in every stage
+    (ff_rcpp: bit-trick estimate + 3 Newton steps). u, v are constant, so one RK4 step of size 1 gives
+    z = sigmoid(u) + 2 sigmoid(v) exactly up to rounding: checked against float64 over arguments that
+    reach both saturations, in the throughput kernel."""
+    monkeypatch.setenv("FF_TUNE_RCP_PAIRS", "1")
+    monkeypatch.setenv("FF_TUNE_RCPP_STAGES", stages)
+    monkeypatch.setenv("FF_TUNE_EXP2P_STEP", "0")
+    sysd = SystemDef("pairs", ["u", "v", "z"], ["0", "0", "sigmoid(u) + 2 * sigmoid(v)"], [])
+    src = FF.ff_emit_source(sysd)
+    assert "sigmoid pairs sharing a reciprocal: 1" in src
+    assert f"stages with the pair reciprocals on the FMA pipe: {stages}" in src
+    assert ("ff_rcpp(" in src.split("ff_rhs_v0", 1)[1]) == (stages == "4")
+    n = 80000 + 3   # enough tiles for the pipe-balanced (throughput) variant
+    ctx = FF.Context(sysd, [n])
+    g = ctx.init_group([-200.0, -200.0, 0.0], [200.0, 200.0, 1.0], n, 1, 0, seed=5)
+    x0 = ctx.read_state(g)
+    x0[2] = 0.0
+    ctx.write_state(g, x0)
+    x0 = x0.astype(np.float64)
+    ctx.step(1, 1.0)
+    got = ctx.read_state(g)
+    sig = lambda a: 0.5 * (1.0 + np.tanh(0.5 * a))   # noqa: E731  (float64, overflow-free)
+    want = sig(x0[0]) + 2 * sig(x0[1])
+    assert np.isfinite(got).all()
+    assert np.abs(got[2] - want).max() <= 1e-6 * 3
+    assert (np.abs(got[2] - want) / np.maximum(want, 1e-3)).max() <= 1e-6

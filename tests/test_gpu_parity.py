@@ -532,11 +532,15 @@ def test_swept_shards_sum_to_whole(mode):
     assert np.array_equal(np.hstack([p[1] for p in parts]).view(np.uint32), sw.view(np.uint32))
 
 
-def test_stn_bifurcation_throughput_variant_sampled():
+@pytest.mark.parametrize("rcpp_stages", [None, "4"])
+def test_stn_bifurcation_throughput_variant_sampled(monkeypatch, rcpp_stages):
     """STN-GPe with w_ss swept over [0, 12) (NEXT 4) at a size that selects the
-    pipe-balanced throughput kernel (both sigmoids of an evaluation share one reciprocal, one
-    exponential per particle-step on the FMA pipe): sampled slices of both groups, including the ragged tail,
-    against the oracle at Tier A after 100 steps."""
+    pipe-balanced throughput kernel (both sigmoids of an evaluation share one reciprocal, on the FMA
+    pipe in one of the four stages): sampled slices of both groups, including the ragged tail,
+    against the oracle at Tier A after 100 steps; also with the shared reciprocal on the FMA pipe
+    (ff_rcpp) in all four stages."""
+    if rcpp_stages:
+        monkeypatch.setenv("FF_TUNE_RCPP_STAGES", rcpp_stages)
     p, s = stn_params()
     n = 50000 + 19
     ctx = FF.Context(s, [n, n])

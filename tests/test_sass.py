@@ -61,20 +61,20 @@ def test_front_end_op_counts():
     import bench
     assert bench.op_counts(systems.lorenz(), -1) == (45, 0, 0, 41, 0, 0)
     assert bench.op_counts(systems.hh_ring(3), -1) == (813, 84, 36, 741, 84, 4)
-    # STN-GPe is MUFU-bound: its two sigmoids share one reciprocal, and 1 of the 8 exponentials of a
-    # particle-step (in one of the four RK4 stages) runs on the FMA pipe
-    assert bench.op_counts(systems.stn_gpe(), -1) == (62, 16, 8, 74, 11, 4)
+    # STN-GPe is MUFU-bound: its two sigmoids share one reciprocal, and in one of the four RK4 stages
+    # that reciprocal runs on the FMA pipe (ff_rcpp)
+    assert bench.op_counts(systems.stn_gpe(), -1) == (62, 16, 8, 73, 11, 4)
 
 
 def test_pipe_balanced_roofline_work():
     """The ALU roofline's work per particle-step: FMA-bound systems keep their FP32 count; a
-    MUFU-bound one gets the least time of both pipes with exponentials movable to the FMA pipe and
-    sigmoid pairs sharing a reciprocal."""
+    MUFU-bound one gets the least time of both pipes with exponentials movable to the FMA pipe,
+    sigmoid pairs sharing a reciprocal and shared reciprocals movable to the FMA pipe."""
     import bench
     assert bench.balanced_work(45, 0, 0) == (45.0, 0, "fma")
     assert bench.balanced_work(813, 84, 36, 4) == (813.0, 0, "fma")
     work, k, pipes = bench.balanced_work(62, 16, 8)
     assert (k, pipes) == (4, "fma+xu") and work == 128 * 12 / 16
-    work, k, pipes = bench.balanced_work(62, 16, 8, 4)
-    assert (k, pipes) == (1, "fma+xu") and work == 128 * 11 / 16
+    work, k, pipes = bench.balanced_work(62, 16, 8, 4)   # pairs, then one reciprocal on the FMA pipe
+    assert (k, pipes) == (0, "fma+xu") and work == 128 * 11 / 16
     assert bench.balanced_work(10, 16, 0) == (128.0, 0, "xu")
