@@ -98,6 +98,46 @@ def test_config4_sweep_16M_rho_y_image():
     assert abs(col.mean() - n / 2048) < 20 and col.min() > 0.9 * n / 2048
 
 
+def test_next4_stn_bifurcation_8M_reset_3d_image():
+    """NEXT row 4 at the bench's size and launch (`bench.py --config stn_bif3d`): 2^22 forward + 2^22
+    backward STN-GPe particles, w_ss swept over [0, 12), reset to the unit square, one fused launch
+    of 100 steps + reset + 3-D binning of (x, y, w_ss) -- the pipe-balanced kernel. Sampled particles
+    the oracle does not reset: Tier A; their reset decision agrees; every channel counts exactly
+    the in-view particles of its group (up to border cases)."""
+    s = systems.stn_gpe()
+    p = np.array([q[1] for q in s.params], np.float32)
+    n = 1 << 22
+    ctx = FF.Context(s, [n, n])
+    gf = ctx.init_group([0.0, 0.0], [1.0, 1.0], n, 1, 0, seed=21)
+    gb = ctx.init_group([0.0, 0.0], [1.0, 1.0], n, -1, 1, seed=22)
+    for g in (gf, gb):
+        ctx.sweep_param(g, "w_ss", 0.0, 12.0, 0, 23)
+    ctx.set_reset(True, [0.0, 0.0], [1.0, 1.0], 0.0)
+    M = views.box_camera([0.0, 0.0, 0.0], [1.0, 1.0, 12.0])
+    img = ctx.project([0, 1, 2], M, 1024, 1024, 2)
+    img.zero_()
+    ctx.step(100, 0.01)
+    rng = np.random.default_rng(72)
+    sv_all = O.sweep_values(0.0, 12.0, 0, 23, 0, n, n)
+    im = ctx.read_image().astype(np.int64)
+    for g, seed, h, ch in ((gf, 21, 0.01, 0), (gb, 22, -0.01, 1)):
+        idx = np.sort(rng.choice(n, 1500, replace=False))
+        idx[-1] = n - 1
+        sv = sv_all[idx]
+        want = oracle_at([0.0, 0.0], [1.0, 1.0], seed, idx, O.STN, p, h, 100, 0, sv)
+        got = sample(ctx, g, idx)
+        ep = np.array([ctx.read_epochs(g, int(i), 1)[0] for i in idx])
+        kept = np.all(np.isfinite(want) & (want >= 0.0) & (want <= 1.0), axis=0)
+        assert np.count_nonzero((ep == 0) != kept) <= 3
+        both = kept & (ep == 0)
+        assert both.sum() > 100
+        assert scaled_error(got[:, both], want[:, both], [1.0, 1.0]).max() <= 1e-5
+        x = ctx.group_view(g).cpu().numpy()
+        assert np.all((x >= 0.0) & (x <= 1.0))             # after the reset every particle is in the box
+        inside, near = in_view_count_3d(np.vstack([x, sv_all[None, :]]), M, 1024, 1024)
+        assert inside <= im[ch].sum() <= inside + near
+
+
 def test_config3_hh_1M():
     s = systems.hh_ring(3)
     d = {p[0]: p[1] for p in s.params}
