@@ -53,6 +53,24 @@ def test_scalar_loop_is_41_ops(lorenz_cubin):
     assert main["FFMA"] + main["FADD"] + main["FMUL"] == 164 and main["LDL"] == 0
 
 
+def test_stn_bifurcation_loop_matches_front_end_count(tmp_path):
+    """The pipe-balanced STN-GPe kernel (w_ss swept, the bench's bifurcation workload) executes what
+    the front end counts and the roofline's generated-work figures report: per particle-step 11 MUFU
+    ops (8 EX2 + 3 RCP: the pair reciprocal of one RK4 stage runs on the FMA pipe) and 73 FP32
+    lane-ops, without spills."""
+    s = systems.stn_gpe()
+    w_ss = [q[0] for q in s.params].index("w_ss")
+    p = tmp_path / "stn.cubin"
+    p.write_bytes(FF.ff_compile_cubin(s, w_ss))
+    loops = [c for c in inner_loops(str(p), "ff_step_p2_t128") if c["MUFU"] >= 8]
+    assert loops, "no RK4 loop found"
+    main = min(loops, key=lambda c: sum(c.values()))
+    # one step per iteration, two particles per thread
+    assert main["MUFU"] == 2 * 11
+    assert 2 * (main["FFMA2"] + main["FMUL2"] + main["FADD2"]) + main["FFMA"] + main["FMUL"] + main["FADD"] == 2 * 73
+    assert main["LDL"] == 0 and main["STL"] == 0
+
+
 def test_front_end_op_counts():
     """Front-end counts per particle-step (4 RHS evaluations + 7 per dimension): the plain
     formulation (the roofline's algorithmic work) and what the kernel executes after the uniform-
