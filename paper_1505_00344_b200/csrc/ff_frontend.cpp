@@ -1191,9 +1191,11 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   // Pipe balancing: a system bound by the MUFU pipe (16 results / clk / SM against 128 FP32 lanes)
   // moves work to the FMA pipe: (1) sigmoids in pairs share one reciprocal (1/dA = dB/(dA dB): one
   // MUFU.RCP instead of two, for 3 FMA-pipe ops), (2) K of the exponentials of a particle-step (4 RHS
-  // evaluations) run as ff_exp2p (8 FMA-pipe ops each). K is split over the 4 RK4 stages (k or k + 1
-  // per stage: two emitted RHS variants), so the balance is set per particle-step, not per
-  // evaluation. Chosen to minimise max(MUFU / 16, FMA / 128) per particle-step (RK4 combination in).
+  // evaluations) run as ff_exp2p (8 FMA-pipe ops each), (3) in R of the 4 RK4 stages the pairs'
+  // shared reciprocals run as ff_rcpp (7 FMA-pipe ops each). K is split over the 4 RK4 stages (k or
+  // k + 1 per stage: two emitted RHS variants; with R > 0 the second variant is k + FMA-pipe
+  // reciprocals instead), so the balance is set per particle-step, not per evaluation. Chosen to
+  // minimise max(MUFU / 16, FMA / 128) per particle-step (RK4 combination in).
   std::vector<int> cand;   // exponentials (exp / sigmoid nodes), in creation order
   std::vector<int> sigs;   // sigmoid nodes
   for (size_t id = 0; id < g.nodes.size(); ++id)
