@@ -66,6 +66,11 @@ def main():
         d = {p[0]: p[1] for p in hh.params}
         ph = np.array([d[k] for k in O.hh_param_names(3)], np.float32)
         run("hh3", hh, O.HH, [-20.0, 0, 0, 0, 0] * 3, [100.0, 1, 1, 1, 1] * 3, 20000, ph, 1, [10, 100, 1000], ppt)
+    # the default (bench) launch at a size that selects the pipe-balanced kernel (FMA-pipe reciprocals)
+    st = systems.stn_gpe()
+    ps = np.array([p[1] for p in st.params], np.float32)
+    run("stn_bif_fwd", st, O.STN, [0, 0], [1, 1], 100000, ps, 1, [100, 1000], 0, sweep=("w_ss", 0.0, 12.0))
+    run("stn_bif_bwd", st, O.STN, [0, 0], [1, 1], 100000, ps, -1, [100], 0, sweep=("w_ss", 0.0, 12.0))
 
 
 if __name__ == "__main__":
