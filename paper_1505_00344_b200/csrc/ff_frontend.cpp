@@ -1116,7 +1116,8 @@ std::vector<float> eval_program(const UProgram& prog, const std::vector<float>& 
   return q;
 }
 
-std::string emit_source(const System& s, int sweep_param, int kernel_select, UProgram* prog, bool balance) {
+std::string emit_source(const System& s, int sweep_param, int kernel_select, UProgram* prog, bool balance,
+                        bool long_launch) {
   if (sweep_param < -1 || sweep_param >= (int)s.param_names.size())
     throw Error(FF_ERR_INVALID_ARG, "sweep parameter index out of range");
   // pass 1: lower once to find exponentials sharing an affine argument c w + d
@@ -1359,10 +1360,13 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   int unroll = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
   int minb_p1 = dim <= 4 ? 4 : (dim <= 8 ? 3 : (dim <= 16 ? 2 : 1));
   int minb_p2 = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
-  // 128-thread packed kernel: for small systems force full occupancy (16 blocks = 64 warps/SM,
-  // <= 32 registers): measured best for Lorenz on B200 (89.6% of the FMA pipe; 12 blocks / 37
-  // registers: 87.9%). tests/test_sass.py checks that the inner loop does not spill.
-  int minb_p2_t128 = dim <= 4 ? 16 : (dim <= 8 ? 4 : 2);
+  // 128-thread packed kernel, small systems: launches of a few steps want full occupancy (16 blocks
+  // = 64 warps/SM, <= 32 registers) to hide the state loads and the histogram reductions; launches
+  // of many steps are FMA-pipe bound and run best with 12 blocks / <= 40 registers (measured on
+  // B200, Lorenz 8.4 M, tools/gpu_run66.sh / gpu_run67.sh: S = 100 7.91 -> 8.06e11, S = 1000
+  // 8.32 -> 8.46e11, S = 10 +1%; S = 1, 2, 4 lose 9%, 5%, 3%). tests/test_sass.py checks that the
+  // inner loops do not spill.
+  int minb_p2_t128 = dim <= 4 ? (long_launch ? 12 : 16) : (dim <= 8 ? 4 : 2);
   if (const char* e = std::getenv("FF_TUNE_MINB_P2_T128")) minb_p2_t128 = std::atoi(e);
   int minb_p4 = dim <= 4 ? 6 : (dim <= 8 ? 2 : 1);   // 128-thread blocks (Lorenz: 76 regs, 6 blocks/SM)
   if (const char* e = std::getenv("FF_TUNE_MINB_P4")) minb_p4 = std::atoi(e);

@@ -47,10 +47,11 @@ struct Module {
   // +6 = the same with position-linear colour compiled in (ff_project_colour), +12 = with the fused
   // image exchange (ff_set_exchange)
   cudaKernel_t exchange = nullptr;  // (in base_lib)
-  // [balanced][id]: balanced = exponentials shared with the FMA pipe (emit_source balance)
-  cudaLibrary_t step_lib[2][12] = {};
-  cudaKernel_t step[2][12] = {};
-  int occ[2][12] = {};
+  // [variant][id]: variant = balanced + 2 long; balanced = exponentials shared with the FMA pipe,
+  // long = the register budget for launches of many steps (emit_source balance, long_launch)
+  cudaLibrary_t step_lib[4][12] = {};
+  cudaKernel_t step[4][12] = {};
+  int occ[4][12] = {};
 };
 
 constexpr int kNumStep = 6;
@@ -167,9 +168,9 @@ struct ff_ctx {
     ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize");  // host buffers go out of scope
   }
 
-  cudaLibrary_t load(int sweep, int ksel, bool bal = true) {
+  cudaLibrary_t load(int sweep, int ksel, bool bal = true, bool long_launch = false) {
     std::vector<char> cubin =
-        ff::compile_cubin(ff::emit_source(sys, sweep, ksel, nullptr, bal), "fireflies_system.cu");
+        ff::compile_cubin(ff::emit_source(sys, sweep, ksel, nullptr, bal, long_launch), "fireflies_system.cu");
     cudaLibrary_t lib = nullptr;
     ck(cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
     return lib;
@@ -187,21 +188,27 @@ struct ff_ctx {
     return modules.emplace(sweep, m).first->second;
   }
 
-  // step kernel `id` (0-11) of the variant, compiled at its first launch
-  cudaKernel_t step_kernel(Module& m, int sweep, int id, bool bal) {
-    if (!m.step[bal][id]) {
-      m.step_lib[bal][id] = load(sweep, id, bal);
+  // step kernel `id` (0-11) of variant v (balanced + 2 long), compiled at its first launch
+  cudaKernel_t step_kernel(Module& m, int sweep, int id, int v) {
+    if (!m.step[v][id]) {
+      m.step_lib[v][id] = load(sweep, id, (v & 1) != 0, (v & 2) != 0);
       const std::string name = std::string(kStepNames[id % kNumStep]) + (id >= kNumStep ? "_c" : "");
-      ck(cudaLibraryGetKernel(&m.step[bal][id], m.step_lib[bal][id], name.c_str()), "cudaLibraryGetKernel(ff_step)");
+      ck(cudaLibraryGetKernel(&m.step[v][id], m.step_lib[v][id], name.c_str()), "cudaLibraryGetKernel(ff_step)");
       int occ = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m.step[bal][id], kStepTPB[id % kNumStep],
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m.step[v][id], kStepTPB[id % kNumStep],
                                                         0) != cudaSuccess) {
         cudaGetLastError();
         occ = 1;
       }
-      m.occ[bal][id] = occ > 0 ? occ : 1;
+      m.occ[v][id] = occ > 0 ? occ : 1;
     }
-    return m.step[bal][id];
+    return m.step[v][id];
+  }
+  // the long-launch register budget differs only for the packed 128-thread kernel of systems of
+  // <= 4 variables (emit_source long_launch); other kernels share the short variant's module
+  int variant_for(bool bal, int id, int64_t n_steps) const {
+    const bool lng = n_steps >= 8 && sys.dim <= 4 && id % kNumStep == 3;
+    return (bal ? 1 : 0) + (lng ? 2 : 0);
   }
   // pipe-balanced (throughput) kernels for launches that fill the GPU; a launch with fewer tiles than
   // two per SM is latency-bound (one particle's RK4 chain is the critical path) and uses MUFU only
@@ -366,8 +373,9 @@ struct ff_ctx {
     const bool colour = image && colour_img;
     const size_t dyn_smem = colour ? 3 * 1024 * sizeof(uint32_t) : 0;
     const int kid = si + (colour ? kNumStep : 0);
-    const cudaKernel_t kern = step_kernel(m, sweep_param, kid, bal);
-    int occ = m.occ[bal][kid];
+    const int var = variant_for(bal, kid, n_steps);
+    const cudaKernel_t kern = step_kernel(m, sweep_param, kid, var);
+    int occ = m.occ[var][kid];
     if (colour) {
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)kern, t, dyn_smem) != cudaSuccess) {
         cudaGetLastError();
@@ -967,7 +975,10 @@ ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* pee
   int pp, tt;
   ctx->default_launch(pp, tt);
   Module& m = ctx->module(ctx->sweep_param);
-  for (int bal = 0; bal < 2; ++bal) ctx->step_kernel(m, ctx->sweep_param, step_index(pp, tt), bal != 0);
+  for (int v = 0; v < 4; ++v) {
+    const int id = step_index(pp, tt);
+    if (ctx->variant_for(v & 1, id, (v & 2) ? 100 : 1) == v) ctx->step_kernel(m, ctx->sweep_param, id, v);
+  }
   // and force the (lazily loaded) exchange kernel in now: a lazy load at its first launch can wait
   // for the device while a peer's exchange kernel spins waiting for this rank (deadlock on one GPU)
   cudaFuncAttributes fa;

@@ -47,6 +47,21 @@ def test_packed_loop_is_41_lane_ops_per_particle_step_no_spills(lorenz_cubin):
     assert main["FFMA"] == 0 and main["FADD"] == 0 and main["FMUL"] == 0   # nothing left unpacked
 
 
+def test_long_launch_register_budget_loop(tmp_path, monkeypatch):
+    """The long-launch build of the packed kernel (12 blocks/SM, <= 40 registers; the runtime uses it
+    for launches of >= 8 steps) keeps the same 164-instruction packed loop, without spills."""
+    monkeypatch.setenv("FF_TUNE_MINB_P2_T128", "12")
+    p = tmp_path / "lorenz12.cubin"
+    p.write_bytes(FF.ff_compile_cubin(systems.lorenz()))
+    loops = [c for c in inner_loops(str(p), "ff_step_p2_t128") if c["FFMA2"] >= 100]
+    main = min(loops, key=lambda c: sum(c.values()))
+    assert main["FFMA2"] + main["FMUL2"] + main["FADD2"] == 164
+    assert main["LDL"] == 0 and main["STL"] == 0
+    res = subprocess.run(["cuobjdump", "-res-usage", str(p)], capture_output=True, text=True).stdout
+    regs = re.search(r"Function ff_step_p2_t128:\s+REG:(\d+)", res)
+    assert regs and 32 < int(regs.group(1)) <= 40
+
+
 def test_scalar_loop_is_41_ops(lorenz_cubin):
     loops = [c for c in inner_loops(lorenz_cubin, "ff_step_p1_t256") if c["FFMA"] >= 100]
     main = min(loops, key=lambda c: sum(c.values()))
