@@ -1357,7 +1357,10 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   for (int i = 0; i < s.dim; ++i) rhs << (i ? ", " : "") << slot[i];
   rhs << "};\n";
   const int dim = s.dim;
-  int unroll = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
+  // RK4 steps per unrolled loop iteration; small systems, measured on B200 (tools/gpu_run70.sh):
+  // FMA-bound Lorenz 2 > 3 > 4 (S = 100: 8.13 / 8.09 / 8.07e11), MUFU-bound STN-GPe 8 > 4 (3.74 /
+  // 3.69e11: more independent MUFU work in flight per warp)
+  int unroll = dim <= 4 ? (n_mufu > 0 ? 8 : 2) : (dim <= 8 ? 2 : 1);
   int minb_p1 = dim <= 4 ? 4 : (dim <= 8 ? 3 : (dim <= 16 ? 2 : 1));
   int minb_p2 = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
   // 128-thread packed kernel, small systems: launches of a few steps want full occupancy (16 blocks
