@@ -1362,7 +1362,9 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   // 3.69e11: more independent MUFU work in flight per warp)
   int unroll = dim <= 4 ? (n_mufu > 0 ? 8 : 2) : (dim <= 8 ? 2 : 1);
   int minb_p1 = dim <= 4 ? 4 : (dim <= 8 ? 3 : (dim <= 16 ? 2 : 1));
-  int minb_p2 = dim <= 4 ? 4 : (dim <= 8 ? 2 : 1);
+  // (small systems run the 256-thread packed kernel for launches of >= 50 steps: 6 blocks / <= 40
+  // registers, tools/gpu_run73.sh)
+  int minb_p2 = dim <= 4 ? 6 : (dim <= 8 ? 2 : 1);
   // 128-thread packed kernel, small systems: launches of a few steps want full occupancy (16 blocks
   // = 64 warps/SM, <= 32 registers) to hide the state loads and the histogram reductions; launches
   // of many steps are FMA-pipe bound and run best with 12 blocks / <= 40 registers (measured on

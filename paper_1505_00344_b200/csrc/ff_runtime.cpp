@@ -270,9 +270,12 @@ struct ff_ctx {
       return;
     }
     // measured on B200: packed pairs win for the paper's systems; 15-D HH needs the
-    // smaller block for its ~248-register pair kernel
+    // smaller block for its ~248-register pair kernel. Small systems: launches of >= 50 steps over
+    // >= 4 tiles of 512 per SM run 256-thread blocks (fewer tile fetches and block barriers per
+    // particle: Lorenz S = 100 8.13 -> 8.22e11), shorter ones 128-thread blocks (S = 10: 5.42 vs 5.34e11)
     ppt_out = ppt ? ppt : (sys.dim <= 16 ? 2 : 1);
-    tpb_out = tpb ? tpb : (sys.dim <= 4 ? 128 : (sys.dim <= 8 ? 256 : 128));
+    const bool wide = n_steps >= 50 && next_slot >= 4 * 512 * (int64_t)nsm;
+    tpb_out = tpb ? tpb : (sys.dim <= 4 ? (wide && ppt_out == 2 ? 256 : 128) : (sys.dim <= 8 ? 256 : 128));
   }
 
   void launch_step(int64_t n_steps, float dt) {
@@ -972,12 +975,13 @@ ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* pee
      "cudaMemsetAsync go flag");
   ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
   // compile / load the step kernel now: no NVRTC or module load between the ranks' first launches
-  int pp, tt;
-  ctx->default_launch(pp, tt);
   Module& m = ctx->module(ctx->sweep_param);
-  for (int v = 0; v < 4; ++v) {
+  for (int64_t n : {1, 10, 100}) {   // the kernels of short, medium and long launches
+    int pp, tt;
+    ctx->default_launch(pp, tt, n);
     const int id = step_index(pp, tt);
-    if (ctx->variant_for(v & 1, id, (v & 2) ? 100 : 1) == v) ctx->step_kernel(m, ctx->sweep_param, id, v);
+    for (int v = 0; v < 4; ++v)
+      if (ctx->variant_for(v & 1, id, (v & 2) ? 100 : 1) == v) ctx->step_kernel(m, ctx->sweep_param, id, v);
   }
   // and force the (lazily loaded) exchange kernel in now: a lazy load at its first launch can wait
   // for the device while a peer's exchange kernel spins waiting for this rank (deadlock on one GPU)
