@@ -1294,6 +1294,7 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   if (prog) {  // the q values as a host program: every uniform node they reach, in creation order
     prog->ops.clear();
     prog->q.clear();
+    prog->mufu_per_step = n_mufu;
     std::map<int, int> at;
     std::function<int(int)> put = [&](int id) -> int {
       auto it = at.find(id);
@@ -1373,7 +1374,10 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   // inner loops do not spill.
   int minb_p2_t128 = dim <= 4 ? (long_launch ? 12 : 16) : (dim <= 8 ? 4 : 2);
   if (const char* e = std::getenv("FF_TUNE_MINB_P2_T128")) minb_p2_t128 = std::atoi(e);
-  int minb_p4 = dim <= 4 ? 6 : (dim <= 8 ? 2 : 1);   // 128-thread blocks (Lorenz: 76 regs, 6 blocks/SM)
+  // 4 particles per thread, 128-thread blocks: 1-4-step launches without an image (memory-bound,
+  // Lorenz 76 registers at 6 blocks/SM); long launches of FMA-bound small systems at 8 blocks /
+  // <= 64 registers (two FFMA2 chains per thread: Lorenz S = 100 8.22 -> 8.41e11, tools/gpu_run76.sh)
+  int minb_p4 = dim <= 4 ? (long_launch ? 8 : 6) : (dim <= 8 ? 2 : 1);
   if (const char* e = std::getenv("FF_TUNE_MINB_P4")) minb_p4 = std::atoi(e);
   // tuning knobs for experiments (not part of the ABI): FF_TUNE_MINB_P2, FF_TUNE_UNROLL
   if (const char* e = std::getenv("FF_TUNE_MINB_P2")) minb_p2 = std::atoi(e);

@@ -73,6 +73,7 @@ struct UProgram {
   struct Op { int kind; double value; int index; int a[3]; };
   std::vector<Op> ops;                  // topological order; kind = front-end node kind
   std::vector<std::pair<int, int>> q;   // per q slot: (op index, negate)
+  int mufu_per_step = 0;                 // MUFU ops per particle-step of the variant (launch choice)
 };
 std::vector<float> eval_program(const UProgram& prog, const std::vector<float>& params);
 

@@ -207,7 +207,7 @@ struct ff_ctx {
   // the long-launch register budget differs only for the packed 128-thread kernel of systems of
   // <= 4 variables (emit_source long_launch); other kernels share the short variant's module
   int variant_for(bool bal, int id, int64_t n_steps) const {
-    const bool lng = n_steps >= 8 && sys.dim <= 4 && id % kNumStep == 3;
+    const bool lng = n_steps >= 8 && sys.dim <= 4 && (id % kNumStep == 3 || id % kNumStep == 5);
     return (bal ? 1 : 0) + (lng ? 2 : 0);
   }
   // pipe-balanced (throughput) kernels for launches that fill the GPU; a launch with fewer tiles than
@@ -252,7 +252,7 @@ struct ff_ctx {
     return groups[gid];
   }
 
-  void default_launch(int& ppt_out, int& tpb_out, int64_t n_steps = 100) const {
+  void default_launch(int& ppt_out, int& tpb_out, int64_t n_steps = 100) {
     // memory-bound launches (1-4 steps, no image) of small systems: 16-byte vector I/O, 4 particles
     // per thread; with an image bound the histogram atomics dominate and the full-occupancy packed
     // kernel below hides them better (measured: 9.0e10 vs 7.8e10 particle-steps/s at S = 1)
@@ -273,8 +273,17 @@ struct ff_ctx {
     // smaller block for its ~248-register pair kernel. Small systems: launches of >= 50 steps over
     // >= 4 tiles of 512 per SM run 256-thread blocks (fewer tile fetches and block barriers per
     // particle: Lorenz S = 100 8.13 -> 8.22e11), shorter ones 128-thread blocks (S = 10: 5.42 vs 5.34e11)
-    ppt_out = ppt ? ppt : (sys.dim <= 16 ? 2 : 1);
     const bool wide = n_steps >= 50 && next_slot >= 4 * 512 * (int64_t)nsm;
+    // FMA-bound small systems (no MUFU op): long launches run 4 particles per thread (two independent
+    // FFMA2 chains, 8 blocks / <= 64 registers): Lorenz S = 10 / 100 / 1000 +4 / +2.3 / +2.8%; a
+    // MUFU-bound one (STN-GPe) loses 6% there (tools/gpu_run76.sh)
+    if (!ppt && !tpb && sys.dim <= 4 && n_steps >= 8 && next_slot >= 4 * 512 * (int64_t)nsm &&
+        uprogram(sweep_param, true).mufu_per_step == 0) {
+      ppt_out = 4;
+      tpb_out = 128;
+      return;
+    }
+    ppt_out = ppt ? ppt : (sys.dim <= 16 ? 2 : 1);
     tpb_out = tpb ? tpb : (sys.dim <= 4 ? (wide && ppt_out == 2 ? 256 : 128) : (sys.dim <= 8 ? 256 : 128));
   }
 
