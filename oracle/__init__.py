@@ -164,13 +164,17 @@ def histogram(x_soa, axes, view, W: int, H: int, C_: int, colour: int, image=Non
     return image
 
 
-def reset(x_soa, bound_lo, bound_hi, t_max, t_now, birth, epoch, ic_lo, ic_hi, seed, first_global=0):
+def reset(x_soa, bound_lo, bound_hi, t_max, t_now, birth, epoch, ic_lo, ic_hi, seed, first_global=0, sweep=None):
     """Apply the reset rule (fireflies_oracle.c) in place to float32 x_soa (dim, n),
-    float32 birth (n) and uint32 epoch (n). bound_lo/hi None = non-finite check only."""
+    float32 birth (n) and uint32 epoch (n). bound_lo/hi None = non-finite check only.
+    sweep = None, or dict(vals=float32 (n) lifted-parameter values (updated in place), lo, hi, mode,
+    seed=sweep seed, n_group=particles in the whole group) -- reset particles redraw the lifted
+    parameter too (reading R16)."""
     L = lib()
     if not hasattr(L, "_reset_sig"):
         L.orc_reset_f32.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_float,
-                                    C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int64]
+                                    C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int64,
+                                    C.c_void_p, C.c_float, C.c_float, C.c_int, C.c_uint64, C.c_int64]
         L.orc_reset_f32.restype = C.c_int
         L._reset_sig = True
     assert x_soa.dtype == np.float32 and x_soa.flags.c_contiguous
@@ -180,11 +184,34 @@ def reset(x_soa, bound_lo, bound_hi, t_max, t_now, birth, epoch, ic_lo, ic_hi, s
     bhi = None if bound_hi is None else np.ascontiguousarray(bound_hi, dtype=np.float32)
     lo = np.ascontiguousarray(ic_lo, dtype=np.float32)
     hi = np.ascontiguousarray(ic_hi, dtype=np.float32)
+    sv, slo, shi, smode, sseed, ngroup = None, 0.0, 0.0, -1, 0, 0
+    if sweep is not None:
+        sv = sweep["vals"]
+        assert sv.dtype == np.float32 and sv.flags.c_contiguous and sv.shape == (n,)
+        slo, shi, smode, sseed = sweep["lo"], sweep["hi"], sweep["mode"], sweep.get("seed", 0)
+        ngroup = sweep.get("n_group", first_global + n)
     rc = L.orc_reset_f32(_ptr(x_soa), n, n, dim, _ptr(blo), _ptr(bhi), t_max, t_now, _ptr(birth), _ptr(epoch),
-                         _ptr(lo), _ptr(hi), seed, first_global)
+                         _ptr(lo), _ptr(hi), seed, first_global, _ptr(sv), slo, shi, smode, sseed, ngroup)
     if rc != 0:
         raise ValueError("orc_reset_f32 rejected its arguments")
     return x_soa
+
+
+def lifted_values(lo: float, hi: float, mode: int, sweep_seed: int, ic_seed: int, dim: int, first: int, count: int,
+                  n_group: int, epoch=None):
+    """Lifted (swept) parameter of particles first..first+count-1 of a group after epoch[j] resets
+    (fireflies_oracle.c orc_lifted_values_f32; readings R13, R16)."""
+    L = lib()
+    L.orc_lifted_values_f32.argtypes = [C.c_float, C.c_float, C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_int64,
+                                        C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+    L.orc_lifted_values_f32.restype = C.c_int
+    ep = None if epoch is None else np.ascontiguousarray(epoch, dtype=np.uint32)
+    assert ep is None or ep.shape == (count,)
+    out = np.empty(count, np.float32)
+    if L.orc_lifted_values_f32(lo, hi, mode, sweep_seed, ic_seed, dim, first, count, n_group, _ptr(ep),
+                               _ptr(out)) != 0:
+        raise ValueError("orc_lifted_values_f32 rejected its arguments")
+    return out
 
 
 def render(image, colours, intensity, radius):

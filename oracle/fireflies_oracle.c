@@ -295,8 +295,47 @@ int orc_histogram_f32(const float* x_soa, int64_t n, int64_t pitch, int dim, con
 }
 
 /* =====================================================================================
- * Reset ("Any trajectories that leave this square region, or which have not been
- * reset for more than time T_max, are reset to a new random set of initial conditions";
+ * Lifted parameter ("we redefine the system so that the bifurcation parameter (w_ss)
+ * is a new state variable, subject to dw_ss/dt = 0. The initial condition range for this new state
+ * variable is set to be the range of parameter values that are of interest"; PAPER.md:95 the same
+ * for Lorenz r; a particle's position "is chosen when the particle is first
+ * initialized (or reset as a result of going out of bounds)"). DESIGN.md readings R13 and R16:
+ * the lifted parameter is component number dim of the particle's extended state. Its value after
+ * e resets of the particle is
+ *   e = 0:            the sweep draw of orc_sweep_values_f32 (mode 0: Philox stream 1 of the
+ *                     sweep seed; mode 1: linspace)
+ *   e >= 1, mode 0:   the lifted component of the e-th reset draw -- word dim % 4 of
+ *                     Philox(ctr {i lo, i hi, dim / 4, 2 + (e - 1)}, key = the group's IC seed),
+ *                     u = (r >> 8) 2^-24, v = uniform_in_box(sw_lo, sw_hi, u)  (as every other
+ *                     component of that draw, see orc_reset_f32)
+ *   e >= 1, mode 1:   unchanged (a linspace sweep is a deterministic grid, not a random initial
+ *                     condition: kept fixed as a deliberate extension of the paper)
+ * ===================================================================================== */
+static float lifted_value(float sw_lo, float sw_hi, int mode, uint64_t sweep_seed, uint64_t ic_seed, int dim,
+                          uint64_t i, int64_t n_group, uint32_t epoch) {
+  if (mode == 0 && epoch > 0) {
+    const uint32_t r = philox_word(ic_seed, i, (uint32_t)(dim / 4), 2u + (epoch - 1u), dim % 4);
+    return uniform_in_box(sw_lo, sw_hi, u01_from_word(r));
+  }
+  if (mode == 0) return uniform_in_box(sw_lo, sw_hi, u01_from_word(philox_word(sweep_seed, i, 0u, 1u, 0)));
+  return uniform_in_box(sw_lo, sw_hi, (float)(((double)i + 0.5) / (double)n_group));
+}
+
+/* Public: lifted-parameter values of particles first .. first+count-1 of a group whose epochs (resets
+ * so far) are epoch[0 .. count-1] (NULL = all 0). */
+int orc_lifted_values_f32(float lo, float hi, int mode, uint64_t sweep_seed, uint64_t ic_seed, int dim, int64_t first,
+                          int64_t count, int64_t n_group, const uint32_t* epoch, float* out) {
+  if (!(lo < hi) || (mode != 0 && mode != 1) || dim < 1 || count < 0 || first < 0 || n_group < 1 ||
+      first + count > n_group)
+    return -1;
+  for (int64_t j = 0; j < count; ++j)
+    out[j] = lifted_value(lo, hi, mode, sweep_seed, ic_seed, dim, (uint64_t)(first + j), n_group, epoch ? epoch[j] : 0u);
+  return 0;
+}
+
+/* =====================================================================================
+ * Reset ("Any trajectories that leave this square region, or which have not been reset for
+ * more than time T_max, are reset to a new random set of initial conditions";
  * per-variable bounds; reading R16). Applied to particles
  * first_global .. first_global + n - 1 of one group (SoA x[d*pitch + j]):
  *   bad = (bounds given ? some component outside [lo_d, hi_d] (NaN counts as outside)
@@ -305,11 +344,17 @@ int orc_histogram_f32(const float* x_soa, int64_t n, int64_t pitch, int dim, con
  *   if bad: e = epoch[j]; epoch[j] = e + 1; birth[j] = t_now;
  *           x_d = uniform_in_box(ic_lo_d, ic_hi_d, u) with u from Philox word d%4 of
  *                 ctr {i lo, i hi, d/4, 2 + e}, key = seed   (stream 2 + e; reading R5)
+ *           and, if the group sweeps a parameter (sweep_vals != NULL), the lifted component
+ *           sweep_vals[j] = lifted_value(..., epoch e + 1) -- component dim of the same draw in
+ *           mode 0, unchanged in mode 1.
  * ===================================================================================== */
 int orc_reset_f32(float* x, int64_t n, int64_t pitch, int dim, const float* bound_lo, const float* bound_hi,
                   float t_max, float t_now, float* birth, uint32_t* epoch, const float* ic_lo, const float* ic_hi,
-                  uint64_t seed, int64_t first_global) {
+                  uint64_t seed, int64_t first_global, float* sweep_vals, float sw_lo, float sw_hi, int sweep_mode,
+                  uint64_t sweep_seed, int64_t n_group) {
   if (dim < 1 || n < 0 || pitch < n || (bound_lo == NULL) != (bound_hi == NULL)) return -1;
+  if (sweep_vals && (!(sw_lo < sw_hi) || (sweep_mode != 0 && sweep_mode != 1) || n_group < first_global + n))
+    return -1;
   const int age_on = t_max > 0.0f && isfinite(t_max);
   for (int64_t j = 0; j < n; ++j) {
     int bad = 0;
@@ -331,6 +376,7 @@ int orc_reset_f32(float* x, int64_t n, int64_t pitch, int dim, const float* boun
       const uint32_t r = philox_word(seed, i, (uint32_t)(d / 4), 2u + e, d % 4);
       x[(int64_t)d * pitch + j] = uniform_in_box(ic_lo[d], ic_hi[d], u01_from_word(r));
     }
+    if (sweep_vals) sweep_vals[j] = lifted_value(sw_lo, sw_hi, sweep_mode, sweep_seed, seed, dim, i, n_group, e + 1u);
   }
   return 0;
 }

@@ -268,3 +268,78 @@ def test_funcs_model_closed_form_at_origin():
     np.testing.assert_allclose(d, [-1 + 0.1 * np.pi, 2 - np.log(2.0), 0.0], atol=1e-15)
     d32 = O.rhs(O.FUNCS, [0.0, 0.0, 0.0], [1.3, 0.7], dtype=np.float32)
     np.testing.assert_allclose(d32, d, atol=1e-6)
+
+
+def test_funcs_model_closed_form_at_nontrivial_points():
+    """Three points where every term is non-zero and has a distinct value: a swapped sin / cos, a
+    wrong pow exponent, a dropped term or a wrong sign changes the result by far more than rounding.
+    The expected values are the model's formulas (fireflies_oracle.c rhs_funcs) evaluated with
+    Python's math module in double precision."""
+    import math as m
+    for (x, y, z), (a, b) in (((0.7, -1.3, 0.4), (1.3, 0.7)), ((-2.1, 0.35, -1.7), (0.5, 2.0)),
+                              ((1.9, 2.6, 0.9), (-0.8, 0.1))):
+        want = [
+            m.sin(a * x) * m.cos(y) + m.tanh(z) - (1 + x * x) ** 0.75 + m.pi * 0.1,
+            m.sqrt(1 + y * y) - m.log(2 + m.sin(x)) + m.exp(-b * x * x) + abs(z - x) - y ** 3 / 10,
+            min(x, y) - max(y, z) / (1 + m.exp(-(x - z))) + (x + y) / (1 + z * z) + m.tan(0.3 * z) - m.e * 0.05 * z,
+        ]
+        got = O.rhs(O.FUNCS, [x, y, z], [a, b])
+        np.testing.assert_allclose(got, want, rtol=1e-13, atol=1e-14)
+        got32 = O.rhs(O.FUNCS, [x, y, z], [a, b], dtype=np.float32)
+        np.testing.assert_allclose(got32, want, rtol=2e-6, atol=2e-6)
+        # and each term matters: perturbing the point changes every component
+        moved = O.rhs(O.FUNCS, [x + 0.01, y - 0.01, z + 0.01], [a, b])
+        assert np.all(np.abs(moved - got) > 1e-4)
+
+
+# ----------------------------------------------------------------------------- HH rate removable singularities
+def _hh_rates(V, dtype=np.float64):
+    """(alpha_m, alpha_n) at membrane potential V from the oracle's HH RHS: with m = n = 0 the gate
+    equations reduce to dm/dt = alpha_m(V), dn/dt = alpha_n(V) (PAPER.md:110-129 gating form)."""
+    p = hh_p(1, I=0.0)
+    x = np.array([V, 0.5, 0.0, 0.0, 0.0], dtype=dtype)
+    d = O.rhs(O.HH, x, p, dtype=dtype)
+    return d[2], d[3]
+
+
+def test_hh_alpha_rates_at_their_removable_singularities():
+    # alpha_m(V) = 0.1 (25 - V) / (exp((25 - V)/10) - 1) -> 0.1 * 10 = 1 at V = 25;
+    # alpha_n(V) = 0.01 (10 - V) / (exp((10 - V)/10) - 1) -> 0.01 * 10 = 0.1 at V = 10 (limit x/(e^(x/y)-1) -> y)
+    am, _ = _hh_rates(25.0)
+    _, an = _hh_rates(10.0)
+    assert am == 1.0 and abs(an - 0.1) < 1e-17
+    am32, _ = _hh_rates(25.0, np.float32)
+    _, an32 = _hh_rates(10.0, np.float32)
+    # float32: 0.01 is not representable; the limit is fl(fl(0.01) * 10), one rounding from 0.1
+    assert am32 == np.float32(1.0) and an32 == np.float32(np.float32(0.01) * np.float32(10.0))
+
+
+@pytest.mark.parametrize("u", [1e-6, -1e-6, 1e-3, -1e-3, 0.05, -0.05, 0.0999, -0.0999])
+def test_hh_vtrap_series_branch_against_expm1(u):
+    """For |u| < 0.1 (u = x/y) the oracle uses the series y (1 - u/2 + u^2/12 - u^4/720) (reading R10).
+    Against x / expm1(x/y) in float64 its relative error must be the first omitted term, u^6/30240
+    (Bernoulli series of u/(e^u - 1)) over the function's value, up to rounding: a wrong coefficient would leave an error of
+    order u^2 or u^4 instead."""
+    for V0, scale in ((25.0, 0.1), (10.0, 0.01)):
+        V = V0 - 10.0 * u
+        x = V0 - V
+        exact = scale * x / np.expm1(x / 10.0)
+        am, an = _hh_rates(V)
+        got = am if V0 == 25.0 else an
+        rel = abs(got - exact) / exact
+        g = u / np.expm1(u)   # exact = scale * 10 * g(u): relative error = (u^6/30240) / g(u)
+        assert rel <= u ** 6 / 30240 / g * 1.02 + 4e-16, (u, rel)
+        if abs(u) <= 1e-3:
+            assert rel <= 1e-12
+
+
+def test_hh_vtrap_continuous_across_the_branch_switch():
+    # both sides of |u| = 0.1 agree with the exact function to the series' truncation error (3.3e-11)
+    for V0 in (25.0, 10.0):
+        for s in (1, -1):
+            vals = []
+            for uu in (0.1 - 1e-12, 0.1 + 1e-12):
+                V = V0 - 10.0 * s * uu
+                a = _hh_rates(V)[0 if V0 == 25.0 else 1]
+                vals.append(a)
+            assert abs(vals[0] - vals[1]) / abs(vals[1]) < 5e-11
