@@ -163,11 +163,12 @@ ff_status ff_get_param(ff_ctx* ctx, const char* name, float* value);
 
 /* Make parameter `name` a per-particle value for group `group_id` (the lifted parameter of
  * a state variable with zero derivative; here it is never integrated, so it is
- * bit-unchanged by construction). mode 0: Philox-uniform in [lo, hi) keyed by `seed`;
+ * bit-unchanged between resets by construction). mode 0: Philox-uniform in [lo, hi) keyed by `seed`;
  * mode 1: linspace lo + (hi - lo) * (i + 0.5) / n_global. At most one parameter per context may
  * be swept (all sweeping groups must name the same one); groups without a sweep use the
- * parameter's current value. The value is recomputed from the particle index in every launch
- * (0 bytes of state). It is addressable as axis index `dim` in ff_project.
+ * parameter's current value. The value is recomputed from the particle index (and, with resets,
+ * its epoch: a mode-0 value is redrawn with the state, see ff_set_reset) in every launch (0 bytes of
+ * state). It is addressable as axis index `dim` in ff_project; ff_read_lifted reads it back.
  * Errors: FF_ERR_UNKNOWN_SYMBOL, FF_ERR_INVALID_ARG (lo >= hi, mode, group), FF_ERR_STATE
  * (another parameter already swept), FF_ERR_COMPILE (variant compile). */
 ff_status ff_sweep_param(ff_ctx* ctx, int group_id, const char* name, float lo, float hi, int mode,
@@ -202,15 +203,30 @@ ff_status ff_step(ff_ctx* ctx, int64_t n_steps, float dt);
  * each particle after its last step, before binning: it is reset if a component is non-finite, or
  * (lo/hi given) outside [lo_d, hi_d], or (t_max > 0 and finite) its simulated time since the last
  * (re)initialisation exceeds t_max. A reset particle gets the group's IC formula (reading R5) with
- * Philox stream 2 + e, e = number of earlier resets of that particle; its swept value is unchanged.
- * lo, hi: HOST arrays of dim floats (both or neither). enable = 0 disables (bookkeeping kept).
- * Allocates library-owned device memory (8 bytes per slot). Call after ff_bind_state; groups created
- * before or after are covered. Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE, FF_ERR_CUDA. */
+ * Philox stream 2 + e, e = number of earlier resets of that particle. A group whose parameter is
+ * swept with mode 0 (Philox) redraws its lifted parameter too: the paper makes it a state variable
+ * whose initial-condition range is the swept range and draws a new position "when
+ * the particle is first initialized (or reset ...)". It is component dim of the same
+ * draw (word dim % 4 of Philox block dim / 4, stream 2 + e; reading R16), so after e
+ * resets a particle's swept value is a function of (IC seed, index, e) and costs no memory beyond the
+ * epoch. A linspace sweep (mode 1) keeps its grid value through resets (a deliberate extension).
+ * lo, hi: HOST arrays of dim floats (both or neither). enable = 0 disables the checks; the per-slot
+ * bookkeeping (epochs, birth times) is allocated at the first enable after ff_bind_state (8 bytes
+ * per slot, library-owned) and kept until the next ff_bind_state, so disabling, re-enabling or
+ * changing the rule never changes a particle's lifted value. Groups created before or after are
+ * covered. Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE, FF_ERR_CUDA. */
 ff_status ff_set_reset(ff_ctx* ctx, int enable, const float* lo, const float* hi, float t_max);
 
 /* Reset counts (epochs) of particles [first, first+count) of a group into a HOST uint32 buffer
  * (synchronous). Errors: FF_ERR_STATE (reset never enabled), FF_ERR_INVALID_ARG. */
 ff_status ff_read_epochs(ff_ctx* ctx, int group_id, int64_t first, int64_t count, uint32_t* host);
+
+/* The lifted (swept) parameter value of particles [first, first+count) of a group into a HOST float
+ * buffer (synchronous): the value the next ff_step integrates and bins them with -- the sweep draw
+ * (ff_sweep_param) after 0 resets, component dim of the latest reset draw otherwise (see
+ * ff_set_reset). Computed on the device by the same routine the step kernel uses (one launch).
+ * Errors: FF_ERR_STATE (no parameter swept), FF_ERR_INVALID_ARG (range), FF_ERR_CUDA. */
+ff_status ff_read_lifted(ff_ctx* ctx, int group_id, int64_t first, int64_t count, float* host);
 
 /* Kernel selection: particles per thread (1, 2 or 4; 2 packs pairs into FFMA2, 4 = two pairs with
  * 16-byte loads) and threads per block (128, 256 or 512; 4 particles only with 128); 0 = library

@@ -23,7 +23,7 @@ FF_MAX_PEERS = 8
 EXPORTS = ["ff_last_error", "ff_abi_version", "ff_build_info", "ff_emit_source", "ff_compile_cubin", "ff_create", "ff_destroy",
            "ff_set_stream", "ff_set_shard", "ff_shard_range", "ff_bind_state", "ff_group_slots", "ff_init_group", "ff_group_info",
            "ff_set_param", "ff_get_param", "ff_sweep_param", "ff_project", "ff_step", "ff_set_reset",
-           "ff_read_epochs", "ff_set_launch",
+           "ff_read_epochs", "ff_read_lifted", "ff_set_launch",
            "ff_read_state", "ff_write_state", "ff_read_image", "ff_render", "ff_project_colour", "ff_launch_count", "ff_sync",
            "ff_set_exchange", "ff_set_grid_limit", "ff_write_state_async", "ff_read_image_async"]
 
@@ -76,6 +76,7 @@ def lib():
             "ff_step": ([P, i64, f32], C.c_int),
             "ff_set_reset": ([P, i32, P, P, f32], C.c_int),
             "ff_read_epochs": ([P, i32, i64, i64, P], C.c_int),
+            "ff_read_lifted": ([P, i32, i64, i64, P], C.c_int),
             "ff_set_launch": ([P, i32, i32], C.c_int),
             "ff_read_state": ([P, i32, i64, i64, P], C.c_int),
             "ff_write_state": ([P, i32, i64, i64, P], C.c_int),

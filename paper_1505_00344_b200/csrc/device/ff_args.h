@@ -96,6 +96,17 @@ struct FFXchgArgs {
   int rank, world;
 };
 
+// Lifted-parameter readback (ff_read_lifted): the swept value of particles [local, local + count) of
+// one group, from their epochs (ff_sweep_value in ff_device.cuh)
+struct FFLiftedArgs {
+  float* out;           // [count] device scratch
+  const ff_u32* epoch;  // per slot, or null (all epochs 0)
+  ff_i64 slot;          // slot of the first particle
+  ff_i64 local;         // group-local index of the first particle
+  ff_i64 count;
+  FFGroup g;            // sweep fields, first_global, n_global, seed
+};
+
 // Render post-process (NEXT row 3): count image -> RGB with sprite falloff.
 #define FF_RENDER_MAX_R 8
 #define FF_RENDER_MAX_C 16

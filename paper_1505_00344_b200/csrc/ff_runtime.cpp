@@ -43,6 +43,7 @@ struct Module {
   cudaLibrary_t base_lib = nullptr;  // ff_init + ff_render
   cudaKernel_t init = nullptr;
   cudaKernel_t render = nullptr;
+  cudaKernel_t lifted = nullptr;     // ff_read_lifted
   // step kernels by (ppt, tpb): 0 p1t128, 1 p1t256, 2 p1t512, 3 p2t128, 4 p2t256, 5 p4t128;
   // +6 = the same with position-linear colour compiled in (ff_project_colour), +12 = with the fused
   // image exchange (ff_set_exchange)
@@ -147,7 +148,7 @@ struct ff_ctx {
 
   // (re)initialise the reset bookkeeping of group gi: epoch 0, birth = current group time, IC box
   void reset_init_group(size_t gi) {
-    if (!reset) return;
+    if (!epoch) return;
     const GroupRec& G = groups[gi];
     const int dim = sys.dim;
     const size_t n = (size_t)(G.slot_end - G.slot_begin);
@@ -185,6 +186,7 @@ struct ff_ctx {
     ck(cudaLibraryGetKernel(&m.init, m.base_lib, "ff_init"), "cudaLibraryGetKernel(ff_init)");
     ck(cudaLibraryGetKernel(&m.render, m.base_lib, "ff_render"), "cudaLibraryGetKernel(ff_render)");
     ck(cudaLibraryGetKernel(&m.exchange, m.base_lib, "ff_exchange"), "cudaLibraryGetKernel(ff_exchange)");
+    ck(cudaLibraryGetKernel(&m.lifted, m.base_lib, "ff_lifted"), "cudaLibraryGetKernel(ff_lifted)");
     return modules.emplace(sweep, m).first->second;
   }
 
@@ -287,6 +289,25 @@ struct ff_ctx {
     tpb_out = tpb ? tpb : (sys.dim <= 4 ? (wide && ppt_out == 2 ? 256 : 128) : (sys.dim <= 8 ? 256 : 128));
   }
 
+  // the group-table fields that identify particles and their lifted parameter (shared by every launch
+  // that evaluates ff_sweep_value)
+  void fill_identity(size_t gi, FFGroup& g) const {
+    const GroupRec& G = groups[gi];
+    g.seed = G.seed;
+    g.slot_begin = G.slot_begin;
+    g.slot_end = G.slot_end;
+    g.n_local = G.n_local;
+    g.first_global = G.first_global;
+    g.n_global = G.n_global;
+    g.colour = G.colour;
+    g.sweep_mode = (sweep_param >= 0) ? G.sweep_mode : -1;
+    g.sweep_seed = G.sw_seed;
+    g.sw_lo = G.sw_lo;
+    g.sw_hi = G.sw_hi;
+    g.sw_top = std::nextafter(G.sw_hi, -INFINITY);
+    g.sw_val = sweep_param >= 0 ? params[sweep_param] : 0.0f;
+  }
+
   void launch_step(int64_t n_steps, float dt) {
     if (groups.empty()) throw ff::Error(FF_ERR_STATE, "no particle groups");
     if (!std::isfinite(dt)) throw ff::Error(FF_ERR_INVALID_ARG, "dt is not finite");
@@ -337,13 +358,8 @@ struct ff_ctx {
       const GroupRec& G = groups[gi];
       FFGroup& g = a.g[gi];
       t_elapsed[gi] += std::fabs((double)dt) * (double)n_steps;
-      g.seed = G.seed;
+      fill_identity(gi, g);
       g.t_now = (float)t_elapsed[gi];
-      g.slot_begin = G.slot_begin;
-      g.slot_end = G.slot_end;
-      g.n_local = G.n_local;
-      g.first_global = G.first_global;
-      g.n_global = G.n_global;
       const float h = (float)G.dir * dt;
       g.h = h;
       g.h2 = h * 0.5f;
@@ -361,13 +377,6 @@ struct ff_ctx {
         q[4] = -q[1];
         q[5] = -q[2];
       }
-      g.colour = G.colour;
-      g.sweep_mode = (sweep_param >= 0) ? G.sweep_mode : -1;
-      g.sweep_seed = G.sw_seed;
-      g.sw_lo = G.sw_lo;
-      g.sw_hi = G.sw_hi;
-      g.sw_top = std::nextafter(G.sw_hi, -INFINITY);
-      g.sw_val = sweep_param >= 0 ? params[sweep_param] : 0.0f;
     }
     for (size_t k = 0; k < params.size(); ++k) a.p[k] = params[k];
     const int64_t tile = (int64_t)p * t;
@@ -666,17 +675,23 @@ ff_status ff_set_reset(ff_ctx* ctx, int enable, const float* lo, const float* hi
     }
   }
   need(!std::isnan(t_max), FF_ERR_INVALID_ARG, "t_max is NaN");
-  ctx->free_reset_buffers();
-  const size_t cap = (size_t)ctx->pitch;
-  ck(cudaMalloc(&ctx->epoch, cap * sizeof(uint32_t)), "cudaMalloc epoch");
-  ck(cudaMalloc(&ctx->birth, cap * sizeof(float)), "cudaMalloc birth");
-  ck(cudaMalloc(&ctx->ic_box, (size_t)FF_MAX_GROUPS * 3 * dim * sizeof(float)), "cudaMalloc ic_box");
+  // the per-slot bookkeeping is allocated once per state binding and kept: the epochs define the
+  // particles' lifted-parameter values (reading R16), so re-enabling or changing the rule must not
+  // restart them
+  const bool fresh = ctx->epoch == nullptr;
+  if (fresh) {
+    const size_t cap = (size_t)ctx->pitch;
+    ck(cudaMalloc(&ctx->epoch, cap * sizeof(uint32_t)), "cudaMalloc epoch");
+    ck(cudaMalloc(&ctx->birth, cap * sizeof(float)), "cudaMalloc birth");
+    ck(cudaMalloc(&ctx->ic_box, (size_t)FF_MAX_GROUPS * 3 * dim * sizeof(float)), "cudaMalloc ic_box");
+  }
   ctx->bound_lo = blo;
   ctx->bound_hi = bhi;
   ctx->t_max = t_max;
   ctx->reset = (lo ? 1 : 0) | ((t_max > 0.0f && std::isfinite(t_max)) ? 2 : 0);
   if (!ctx->reset) ctx->reset = 4;  // non-finite check only
-  for (size_t gi = 0; gi < ctx->groups.size(); ++gi) ctx->reset_init_group(gi);
+  if (fresh)
+    for (size_t gi = 0; gi < ctx->groups.size(); ++gi) ctx->reset_init_group(gi);
   FF_CATCH
 }
 
@@ -692,6 +707,37 @@ ff_status ff_read_epochs(ff_ctx* ctx, int group_id, int64_t first, int64_t count
                        cudaMemcpyDeviceToHost, ctx->stream), "cudaMemcpyAsync epochs");
     ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
   }
+  FF_CATCH
+}
+
+ff_status ff_read_lifted(ff_ctx* ctx, int group_id, int64_t first, int64_t count, float* host) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  const GroupRec& g = ctx->group(group_id);
+  need(ctx->sweep_param >= 0, FF_ERR_STATE, "no parameter is swept");
+  need(host || count == 0, FF_ERR_INVALID_ARG, "host buffer is NULL");
+  need(first >= 0 && count >= 0 && first + count <= g.n_local, FF_ERR_INVALID_ARG, "particle range out of bounds");
+  if (count == 0) return FF_OK;
+  Module& m = ctx->module(ctx->sweep_param);
+  FFLiftedArgs a;
+  std::memset(&a, 0, sizeof a);
+  ctx->fill_identity((size_t)group_id, a.g);
+  a.epoch = ctx->epoch;
+  a.slot = g.slot_begin + first;
+  a.local = first;
+  a.count = count;
+  ck(cudaMallocAsync(reinterpret_cast<void**>(&a.out), (size_t)count * sizeof(float), ctx->stream), "cudaMallocAsync");
+  void* args[] = {&a};
+  const cudaError_t le = cudaLaunchKernel((const void*)m.lifted, dim3((unsigned)((count + 255) / 256)), dim3(256), args,
+                                         0, ctx->stream);
+  cudaError_t ce = cudaSuccess;
+  if (le == cudaSuccess)
+    ce = cudaMemcpyAsync(host, a.out, (size_t)count * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream);
+  cudaFreeAsync(a.out, ctx->stream);
+  ck(le, "launch ff_lifted");
+  ck(ce, "cudaMemcpyAsync lifted");
+  ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+  ++ctx->launches;
   FF_CATCH
 }
 

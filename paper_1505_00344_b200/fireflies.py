@@ -138,6 +138,12 @@ def ff_read_epochs(ctx, group_id: int, first: int, count: int) -> np.ndarray:
     return out
 
 
+def ff_read_lifted(ctx, group_id: int, first: int, count: int) -> np.ndarray:
+    out = np.empty(count, dtype=np.float32)
+    check(lib().ff_read_lifted(ctx, group_id, first, count, _fptr(out)))
+    return out
+
+
 def ff_set_launch(ctx, particles_per_thread: int = 0, threads_per_block: int = 0):
     check(lib().ff_set_launch(ctx, particles_per_thread, threads_per_block))
 
@@ -148,8 +154,11 @@ def ff_read_state(ctx, group_id: int, first: int, count: int, dim: int) -> np.nd
     return out
 
 
-def ff_write_state(ctx, group_id: int, first: int, host_soa) -> None:
+def ff_write_state(ctx, group_id: int, first: int, host_soa, dim: int) -> None:
     a = np.ascontiguousarray(host_soa, dtype=np.float32)
+    # the library copies dim rows of a.shape[1] floats from this buffer: the shape must be (dim, count)
+    if a.ndim != 2 or a.shape[0] != dim:
+        raise ValueError(f"host_soa must have shape (dim={dim}, count), got {a.shape}")
     check(lib().ff_write_state(ctx, group_id, first, a.shape[1], _fptr(a)))
 
 
@@ -281,6 +290,11 @@ class Context:
         count = n - first if count is None else count
         return ff_read_epochs(self.ctx, g, first, count)
 
+    def read_lifted(self, g, first=0, count=None):
+        _, n, _ = ff_group_info(self.ctx, g)
+        count = n - first if count is None else count
+        return ff_read_lifted(self.ctx, g, first, count)
+
     def set_launch(self, ppt=0, tpb=0):
         ff_set_launch(self.ctx, ppt, tpb)
 
@@ -290,7 +304,7 @@ class Context:
         return ff_read_state(self.ctx, g, first, count, self.dim)
 
     def write_state(self, g, host_soa, first=0):
-        ff_write_state(self.ctx, g, first, host_soa)
+        ff_write_state(self.ctx, g, first, host_soa, self.dim)
 
     def read_image(self):
         """Host copy of the bound image as uint32 (C, H, W)."""

@@ -115,13 +115,19 @@ def test_stn_bifurcation_3d_pipeline():
     for g, seed, h, ch in ((gf, 21, 0.01, 0), (gb, 22, -0.01, 1)):
         x = O.rk4(O.STN, O.ic_uniform([0, 0], [1, 1], seed, 0, n), p, np.float32(h), 100, 0, sv)
         b, e = np.zeros(n, np.float32), np.zeros(n, np.uint32)
-        O.reset(x, [0, 0], [1, 1], 0.0, t, b, e, [0, 0], [1, 1], seed)
+        svg = sv.copy()   # reset particles redraw their w_ss too (reading R16)
+        O.reset(x, [0, 0], [1, 1], 0.0, t, b, e, [0, 0], [1, 1], seed,
+                sweep=dict(vals=svg, lo=0.0, hi=12.0, mode=0, seed=23, n_group=n))
         got, ge = ctx.read_state(g), ctx.read_epochs(g)
         same = ge == e
         assert (~same).sum() <= 3
         err = scaled_error(got[:, same], x[:, same], [1.0, 1.0])
         assert err.max() <= 1e-5
-        O.histogram(x, [0, 1, 2], M, 256, 256, 2, ch, image=want_img, sweep_vals=sv)
+        lifted = ctx.read_lifted(g)
+        assert np.array_equal(lifted[same].view(np.uint32), svg[same].view(np.uint32))
+        if ch == 1:
+            assert (e > 0).mean() > 0.5 and np.any(svg != sv)   # backward particles escape and redraw
+        O.histogram(x, [0, 1, 2], M, 256, 256, 2, ch, image=want_img, sweep_vals=svg)
     got_img = ctx.read_image().astype(np.int64)
     # particles near a pixel edge (or with a different reset decision) may land one bin apart
     assert np.abs(got_img - want_img.astype(np.int64)).sum() <= 2 * 40
@@ -140,3 +146,98 @@ def test_reset_then_binning_sees_new_positions():
         img.zero_()
         ctx.step(100, 0.01)
         assert int(ctx.read_image().sum()) == n
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_lifted_values_readback_epoch0(mode):
+    # before any reset the lifted value is the sweep draw (reading R13), bit-exact
+    s, _ = stn_params()
+    n = 5000 + 3
+    ctx = FF.Context(s, [n])
+    g = ctx.init_group([0, 0], [1, 1], n, 1, 0, seed=9)
+    ctx.sweep_param(g, "w_ss", 0.0, 12.0, mode, 31)
+    want = O.sweep_values(0.0, 12.0, mode, 31, 0, n, n)
+    assert np.array_equal(ctx.read_lifted(g).view(np.uint32), want.view(np.uint32))
+    ctx.set_reset(True, [0.0, 0.0], [1.0, 1.0], 0.0)   # bookkeeping exists, every epoch 0
+    assert np.array_equal(ctx.read_lifted(g).view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("ppt,tpb", [(1, 128), (2, 256), (4, 128)])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_reset_redraws_lifted_parameter(ppt, tpb, mode):
+    """PAPER.md:54 / :207: the swept parameter is a state variable whose IC range is the sweep range,
+    and a reset draws a new position -- so a reset particle gets a new w_ss (mode 0), bit-exact vs
+    the oracle's reset rule; non-reset particles keep theirs; the state keeps Tier A with the new
+    values; the fused image bins (x, w_ss) with them. Linspace sweeps (mode 1) keep their grid value."""
+    s, p = stn_params()
+    n, S, seed, sseed = 8000 + 13, 50, 22, 23
+    ctx = FF.Context(s, [n])
+    ctx.set_launch(ppt, tpb)
+    g = ctx.init_group([0, 0], [1, 1], n, -1, 0, seed=seed)
+    ctx.sweep_param(g, "w_ss", 0.0, 12.0, mode, sseed)
+    ctx.set_reset(True, [0.0, 0.0], [1.0, 1.0], 0.0)
+    view = [0.0, 1.0, 0.0, 12.0]
+    img = ctx.project([0, 2], view, 128, 96, 1)
+    x = O.ic_uniform([0, 0], [1, 1], seed, 0, n)
+    sv = O.sweep_values(0.0, 12.0, mode, sseed, 0, n, n)
+    sv0 = sv.copy()
+    b, e = np.zeros(n, np.float32), np.zeros(n, np.uint32)
+    t = 0.0
+    for launch in range(3):
+        img.zero_()
+        ctx.step(S, 0.01)
+        t += abs(float(np.float32(0.01))) * S
+        x = O.rk4(O.STN, x, p, np.float32(-0.01), S, 0, sv)
+        e_before = e.copy()
+        O.reset(x, [0, 0], [1, 1], 0.0, np.float32(t), b, e, [0, 0], [1, 1], seed,
+                sweep=dict(vals=sv, lo=0.0, hi=12.0, mode=mode, seed=sseed, n_group=n))
+        got, ge, lifted = ctx.read_state(g), ctx.read_epochs(g), ctx.read_lifted(g)
+        # the GPU's lifted values are the oracle's function of the GPU's own epochs, for every particle
+        want_l = O.lifted_values(0.0, 12.0, mode, sseed, seed, 2, 0, n, n, ge)
+        assert np.array_equal(lifted.view(np.uint32), want_l.view(np.uint32))
+        same = ge == e
+        assert (~same).sum() <= max(2, n // 1000)
+        assert np.array_equal(lifted[same].view(np.uint32), sv[same].view(np.uint32))
+        fresh = same & (e != e_before)
+        assert np.array_equal(got[:, fresh].view(np.uint32), x[:, fresh].view(np.uint32))
+        if mode == 1:
+            assert np.array_equal(lifted.view(np.uint32), sv0.view(np.uint32))
+        elif launch == 0:
+            assert np.all(lifted[fresh] != sv0[fresh]) and fresh.sum() > n // 4
+        keep = same & (e == e_before)
+        err = scaled_error(got[:, keep], x[:, keep], [1.0, 1.0])
+        assert err.size == 0 or err.max() <= 1e-5
+        # fused image of (x, w_ss) after the reset == the oracle's binning of the GPU's state and lifted
+        # values (P3: identical coordinates -> bit-exact)
+        want_img = O.histogram(got, [0, 2], view, 128, 96, 1, 0, sweep_vals=lifted)
+        assert np.array_equal(ctx.read_image(), want_img)
+        x[:, ~same], e[~same], sv[~same] = got[:, ~same], ge[~same], lifted[~same]   # resync (test logic)
+    # disabling and re-enabling the reset rule keeps every particle's lifted value
+    before = ctx.read_lifted(g)
+    ctx.set_reset(False)
+    ctx.set_reset(True, [0.0, 0.0], [1.0, 1.0], 0.0)
+    assert np.array_equal(ctx.read_lifted(g).view(np.uint32), before.view(np.uint32))
+
+
+def test_lifted_redraw_uses_a_second_philox_block_at_dim_4():
+    # a 4-variable system: the lifted component is word 0 of Philox block 1 (tests/golden reset_golden)
+    import json
+    import os
+    doc = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reset_golden.json")))
+    case = [c for c in doc["cases"] if len(c["lo"]) == 4][0]
+    from paper_1505_00344_b200.systems import SystemDef
+    sysdef = SystemDef("lin4", ["a", "b", "c", "d"], ["k*a", "k*b", "k*c", "k*d"], [("k", 0.0, None, None)])
+    n = case["index"] + 1
+    ctx = FF.Context(sysdef, [n])
+    g = ctx.init_group(case["lo"], case["hi"], n, 1, 0, seed=case["seed"])
+    ctx.sweep_param(g, "k", case["sweep"][0], case["sweep"][1], 0, 77)
+    ctx.set_reset(True)
+    for r in range(case["reset"] + 1):   # poison the particle once per launch: e resets -> epoch e + 1
+        st = ctx.read_state(g)
+        st[:, case["index"]] = np.nan
+        ctx.write_state(g, st)
+        ctx.step(1, 0.0)
+    assert ctx.read_epochs(g)[case["index"]] == case["reset"] + 1
+    got = ctx.read_state(g)[:, case["index"]]
+    assert ["%08x" % v for v in got.view(np.uint32)] == case["bits"]
+    assert "%08x" % ctx.read_lifted(g)[case["index"]:].view(np.uint32)[0] == case["lifted_bits"]
