@@ -38,8 +38,9 @@ XU_LANES = 16     # MUFU results per clock per SM (same microbenchmark)
 WORKLOADS = {
     "lorenz3d": dict(system="lorenz", groups=[(1 << 22, 1, 0, 2), (1 << 22, -1, 1, 3)], params={"r": 28.0},
                      box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj="lorenz_camera", W=1024, H=1024, C=2,
-                     S=100, dt=0.01,
-                     desc="Lorenz r=28, 4M fwd + 4M bwd, 3-D perspective image 1024x1024x2"),
+                     S=100, dt=0.01, reset=(None, None, 0.0),
+                     desc="Lorenz r=28, 4M fwd + 4M bwd, 3-D perspective image 1024x1024x2, non-finite "
+                          "particles reset (PAPER.md:42, :204)"),
     "stn": dict(system="stn_gpe", groups=[(5000, 1, 0, 1), (5000, -1, 1, 11)], params={},
                 box=([0.0, 0.0], [1.0, 1.0]), proj=([0, 1], [0.0, 1.0, 0.0, 1.0]), W=512, H=512, C=2,
                 S=1000, dt=0.01, 
@@ -64,8 +65,8 @@ WORKLOADS = {
                            "(PAPER.md:54, :59; NEXT row 4)"),
     "lorenz1b": dict(system="lorenz", groups=[(1 << 30, 1, 0, 6)], params={"r": 28.0}, strong=True,
                      box=([-10.0, -30.0, 0.0], [10.0, 30.0, 50.0]), proj="lorenz_camera", W=1024, H=1024, C=1,
-                     S=100, dt=0.01,
-                     desc="Lorenz 1B particles sharded over the GPUs (configs[4])"),
+                     S=100, dt=0.01, reset=(None, None, 0.0),
+                     desc="Lorenz 1B particles sharded over the GPUs (configs[4]), non-finite particles reset"),
 }
 
 
@@ -156,7 +157,7 @@ def setup(args, w, rank, world):
         name, a, b, mode, seed = w["sweep"]
         for g in gids:
             ctx.sweep_param(g, name, a, b, mode, seed)
-    if "reset" in w:
+    if "reset" in w and not args.no_reset:
         ctx.set_reset(True, *w["reset"])
     if w.get("prerun"):
         ctx.step(w["prerun"], w["dt"])
@@ -245,9 +246,9 @@ def run_ours(args, w, rank, world, device):
             img.zero_()
             ev[i][1].record(stream)
             ctx.step(S, w["dt"])
-            ev[i][2].record(stream)
-            if reduce:
+            if reduce:   # the image sum is part of the frame: it ends before the frame's end event
                 torch.distributed.all_reduce(img)
+            ev[i][2].record(stream)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
     if dist:
@@ -342,6 +343,16 @@ PAIR_OPS = 3    # FMA-pipe ops that let two sigmoids share one reciprocal (one M
 RCPP_OPS = 7    # FMA-pipe ops of a pair reciprocal computed on the FMA pipe (ff_rcpp in ff_device.cuh)
 
 
+# L_alg, frozen per system: (FP32 FMA-pipe lane-ops, MUFU ops) per particle-step of
+# the plain formulation, a*b+c counted once. Lorenz: 44, the survey's probe of the straight-line RK4
+# (216 FFMA + 80 FADD + 58 FMUL per 8 steps; the front end's plain lowering counts 45, one contraction
+# fewer). STN-GPe and HH ring (N = 3): the front end's plain count of the RHS as written (no gating
+# rewrite, uniform factors multiplied in every evaluation, every exponential and reciprocal on MUFU,
+# no exponential sharing), frozen here; tests/test_bench_contract.py checks the front end still
+# agrees. HH: 825 + 132 MUFU (11 exponentials per neuron and evaluation, SURVEY.md:36).
+L_ALG = {"lorenz": (44, 0), "stn_gpe": (62, 16), "hh_ring3": (825, 132)}
+
+
 def op_counts(sysdef, sweep_idx):
     """Work per particle-step: (algorithmic FMA-pipe lane-ops, algorithmic MUFU ops, exponentials,
     generated FMA-pipe lane-ops, generated MUFU ops, sigmoid pairs).
@@ -355,7 +366,7 @@ def op_counts(sysdef, sweep_idx):
     import paper_1505_00344_b200 as FF
     src = FF.ff_emit_source(sysdef, sweep_idx)
     m = re.search(r"per particle-step, 4 evaluations \(front-end count\): (\d+) arithmetic ops, (\d+) MUFU ops", src)
-    p = re.search(r"plain formulation \(no gating rewrite, uniform factors multiplied in every evaluation\): "
+    p = re.search(r"plain formulation \(no gating rewrite, uniform factors multiplied in every evaluation, no exponential sharing\): "
                   r"(\d+) arithmetic ops, (\d+) MUFU ops, (\d+) exponentials, (\d+) sigmoid pairs", src)
     return (4 * int(p.group(1)) + 7 * sysdef.dim, 4 * int(p.group(2)), 4 * int(p.group(3)),
             int(m.group(1)) + 7 * sysdef.dim, int(m.group(2)), 4 * int(p.group(4)))
@@ -449,6 +460,25 @@ def reference_sample_size(w, S):
     return max(1024, int(per * 100 / S))
 
 
+def relaunch(n):
+    """`python bench.py --gpus N` without torchrun: re-run this command under torch.distributed.run,
+    one rank per GPU on 127.0.0.1 (the driver's own launch), after checking N GPUs are visible.
+    Returns torchrun's exit code."""
+    import socket
+    import subprocess
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}", file=sys.stderr)
+        return 1
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -464,14 +494,20 @@ def main():
     ap.add_argument("--flush", default="read", choices=["read", "memset", "none"],
                     help="L2 flush between timed frames (default: read 256 MiB; 'none' only for experiments)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "fused"],
-                    help="per-frame image sum over ranks (N > 1): the library's exchange over peer memory "
-                         "after each launch (ff_set_exchange; 'auto' validates it once and falls back to NCCL), "
-                         "or an NCCL all-reduce")
+    ap.add_argument("--no-reset", action="store_true", help="(experiments) leave the workload's reset rule off")
+    ap.add_argument("--exchange", default="nccl", choices=["auto", "nccl", "fused"],
+                    help="per-frame image sum over ranks (N > 1): an NCCL all-reduce (default), or the "
+                         "library's exchange over peer memory after each launch (ff_set_exchange; 'auto' "
+                         "validates it once and falls back to NCCL) -- not the default until it has run "
+                         "across physical GPUs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = WORKLOADS[args.config]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(relaunch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and world != args.gpus and os.environ.get("FF_BENCH_ONE_DEVICE") != "1":
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     S = args.S or w["S"]
@@ -496,7 +532,8 @@ def main():
                 "steps": len(vals), "warmup": args.warmup, "ms_per_step": n * S / v * 1e3, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": v, "unit": "particle-steps/s", "cores": threads, "kind": "oracle",
-                                 "sample": sample},
+                                 "sample": sample, "build": "scalar oracle, gcc -O2 -ffp-contract=off, OpenMP "
+                                                             "over particles, no SIMD (not a tuned CPU code)"},
                 "e2e": {"value": v, "unit": "particle-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -515,6 +552,10 @@ def main():
             torch.distributed.init_process_group(backend)
     device = torch.device("cuda", local_rank)
     torch.cuda.set_device(device)
+    if world > 1:   # one line per rank on stderr: which GPU each rank drives (stdout holds the JSON line)
+        nccl = ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else "-"
+        print(f"bench.py: rank {rank}/{world} on cuda:{local_rank} ({torch.cuda.get_device_name(device)}, "
+              f"{backend}, NCCL {nccl})", file=sys.stderr, flush=True)
     r = run_ours(args, w, rank, world, device)
     if world > 1:
         config["parallelism"] = f"particles sharded over {world} GPU(s), " + (
@@ -539,9 +580,12 @@ def main():
     # executes 41). The ALU roofline is pipe-balanced (balanced_work): FMA-bound systems report against
     # the FP32 peak as before; a MUFU-bound one against the least time both pipes together need.
     sysdef = make_system(w["system"])
-    fma_ops, mufu_ops, n_exp, gen_ops, gen_mufu, n_pairs = op_counts(sysdef, r["sweep_idx"])
+    _, _, n_exp, gen_ops, gen_mufu, n_pairs = op_counts(sysdef, r["sweep_idx"])
+    fma_ops, mufu_ops = L_ALG[w["system"]]
     work, k_bal, alu_pipes = balanced_work(fma_ops, mufu_ops, n_exp, n_pairs)
     dim = sysdef.dim
+    rate = per_launch / kern_s   # particle-steps/s of the step kernel
+    fma_peak, xu_peak = N_SM * FMA_LANES * f_max, N_SM * XU_LANES * f_max
     cands = {
         "alu": (per_launch * work / kern_s, N_SM * FMA_LANES * f_max,
                 "Tops/s (FP32-pipe-equivalent lane-ops of the pipe-balanced work, a*b+c = 1 op)",
@@ -562,6 +606,10 @@ def main():
                      "balanced_exponentials_on_fma": k_bal,
                      "generated_fma_ops": gen_ops, "generated_mufu_ops": gen_mufu},
             "fracs_all_pipes": fracs,
+            # per pipe: L_alg at the kernel's rate (algorithmic) and the executed op counts (what the
+            # pipe actually did; the front end's savings show as algorithmic > executed)
+            "pipes": {"fma": {"algorithmic_frac": rate * fma_ops / fma_peak, "executed_frac": rate * gen_ops / fma_peak},
+                      "xu": {"algorithmic_frac": rate * mufu_ops / xu_peak, "executed_frac": rate * gen_mufu / xu_peak}},
             "kernel": "ff_step (integrate S steps + project + count, one launch)"}
     roof["traffic"] = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -575,7 +623,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": r["t_total_ms"] / args.steps, "higher_is_better": True,
             "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Philox ICs from the paper's IC boxes)", "config": config,
-            "pct_fp32_peak": 100 * fracs["alu"],
+            "pct_fp32_peak": 100 * rate * gen_ops / fma_peak,   # executed FMA-pipe ops (<= 100 by construction)
             "roofline": roof, "clocks": clocks, "gpu_launches": r["launches"], "e2e": r["e2e"],
             "kernel_ms_mean": r["kern_ms"], "frame_ms_p10_p50_p90": [float(np.percentile(r["frame_ms"], q))
                                                                      for q in (10, 50, 90)],
@@ -587,6 +635,9 @@ def main():
         line["cpu_baseline"] = {"value": v, "unit": "particle-steps/s", "cores": threads, "kind": "oracle",
                                 "sample": f"{n} particles x {r['S']} RK4 steps + binning ({dt:.1f} s)",
                                 "host_cpu": host_cpu_model(),
+                                "build": "the scalar oracle as it stands (plain C, gcc -O2 -ffp-contract=off, "
+                                         "OpenMP over particles, no SIMD): a correctness reference, not a tuned "
+                                         "CPU implementation -- the GPU/CPU ratio is context only",
                                 "single_core": single_core_oracle(args.config, max(1024, n // 32), r["S"])}
     print(json.dumps(line))
 

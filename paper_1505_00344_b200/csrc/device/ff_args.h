@@ -55,6 +55,8 @@ struct FFStepArgs {
   int axes[3];
   float view[16];
   float s0, s1;         // 2-D scales W/(hi0-lo0), H/(hi1-lo1), computed by the host in float
+  float fW, fH, hW, hH; // (float)W, (float)H, W * 0.5f, H * 0.5f (exact; host-computed)
+  int ax_id;            // 1: axes[j] == j for every projected axis (no per-particle axis selection)
   int n_groups;
   // device-side reset (NEXT row 1): 0 off, else bit 1 = bounds, bit 2 = age
   int reset;

@@ -1143,12 +1143,11 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
       if (best_n >= 2) plan[kv.first] = best_c0;
     }
   }
-  // the plain formulation's op count (no gating rewrite, no factored scales): the fixed algorithmic
-  // work per evaluation that bench.py's roofline counts
+  // the plain formulation's op count (no gating rewrite, no factored scales, no exponential
+  // sharing): the fixed algorithmic work per evaluation that bench.py's roofline counts
   int n_arith_plain = 0, n_mufu_plain = 0, n_exp_plain = 0, n_sig_plain = 0;
   {
     Dag gp(sweep_param);
-    gp.plan = &plan;
     gp.gating = false;
     std::vector<int> rp;
     for (int i = 0; i < s.dim; ++i) rp.push_back(gp.lower(s.rhs[i]));
@@ -1310,7 +1309,14 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   std::ostringstream rhs;
   rhs << "// Generated right-hand side (" << s.dim << " state variables, " << s.param_names.size()
       << " parameters, swept parameter index " << sweep_param << ").\n";
-  for (int i = 0; i < s.dim; ++i) rhs << "//   d" << s.var_names[i] << "/dt = " << s.rhs_text[i] << "\n";
+  // (user text goes into // comments: control characters -- a multi-line expression's newlines --
+  // become spaces so nothing leaks out of the comment into the source)
+  auto one_line = [](std::string t) {
+    for (char& ch : t)
+      if (static_cast<unsigned char>(ch) < 0x20 || ch == 0x7f) ch = ' ';
+    return t;
+  };
+  for (int i = 0; i < s.dim; ++i) rhs << "//   d" << s.var_names[i] << "/dt = " << one_line(s.rhs_text[i]) << "\n";
   for (size_t k = 0; k < s.param_names.size(); ++k)
     rhs << "//   a.p[" << k << "] = " << s.param_names[k]
         << ((int)k == sweep_param ? "  (swept: the per-particle value sw is used instead)" : "") << "\n";
@@ -1319,7 +1325,7 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   rhs << "// exponentials on the FMA pipe per particle-step (pipe balancing): " << K
       << "; sigmoid pairs sharing a reciprocal: " << (use_pairs ? (int)pairs.size() / 2 : 0)
       << "; stages with the pair reciprocals on the FMA pipe: " << R << "\n";
-  rhs << "// plain formulation (no gating rewrite, uniform factors multiplied in every evaluation): "
+  rhs << "// plain formulation (no gating rewrite, uniform factors multiplied in every evaluation, no exponential sharing): "
       << n_arith_plain << " arithmetic ops, " << n_mufu_plain << " MUFU ops, " << n_exp_plain << " exponentials, "
       << n_sig_plain / 2 << " sigmoid pairs\n";
   auto emit_rhs = [&](const std::string& fname, SignSelect& ss, const std::vector<std::string>& o) {
@@ -1394,6 +1400,9 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   pre << "#define FF_MINB_P4 " << minb_p4 << "\n";
   pre << "#define FF_SWEEP " << sweep_param << "\n";
   pre << "#define FF_KSEL " << kernel_select << "\n";
+  int prefetch = 0;
+  if (const char* e = std::getenv("FF_TUNE_PREFETCH")) prefetch = std::atoi(e);
+  pre << "#define FF_PREFETCH " << prefetch << "\n";
 
   std::string tmpl(kDeviceTemplate);
   const std::string marker = "#include_generated_rhs";

@@ -21,7 +21,7 @@
 static_assert(sizeof(FFGroup) == 120, "FFGroup layout");
 static_assert(FF_MAX_SCALED_ == FF_MAX_SCALED, "scaled-component table size");
 static_assert(FF_MAX_DERIVED_ == FF_MAX_DERIVED, "derived-value table size");
-static_assert(offsetof(FFStepArgs, g) == 744, "FFStepArgs layout");
+static_assert(offsetof(FFStepArgs, g) == 768, "FFStepArgs layout");
 static_assert(FF_MAX_PEERS_ == FF_MAX_PEERS, "peer table size");
 static_assert(FF_MAX_DIM_ == FF_MAX_DIM, "bounds table size");
 static_assert(FF_MAX_GROUPS_ == FF_MAX_GROUPS, "group table size");
@@ -339,6 +339,12 @@ struct ff_ctx {
     std::memcpy(a.view, view, sizeof view);
     a.s0 = s0;
     a.s1 = s1;
+    a.fW = (float)W;
+    a.fH = (float)H;
+    a.hW = (float)W * 0.5f;
+    a.hH = (float)H * 0.5f;
+    a.ax_id = 1;
+    for (int j = 0; j < proj; ++j) a.ax_id &= axes[j] == j;
     a.n_groups = (int)groups.size();
     a.reset = n_steps > 0 ? reset : 0;
     a.t_max = t_max;
@@ -408,13 +414,15 @@ struct ff_ctx {
     if (grid_limit > 0 && grid_limit < resident) resident = grid_limit;
     const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
     // static tile rounds for 1-2-step launches (ff_step_body): all but the last round of tiles
-    const int64_t ns = (n_steps <= 2 && sys.dim <= 8 && ntiles / grid >= 2) ? ntiles / grid - 1 : 0;
-    a.static_rounds = (int)ns;
+    int64_t ns = (n_steps <= 2 && sys.dim <= 8 && ntiles / grid >= 2) ? ntiles / grid - 1 : 0;
+    static const int all_static_max = std::getenv("FF_TUNE_STATIC_ALL") ? std::atoi(std::getenv("FF_TUNE_STATIC_ALL")) : 0;
+    const bool all_static = sys.dim <= 8 && n_steps <= all_static_max;
+    a.static_rounds = all_static ? -1 : (int)ns;
     void* args[] = {&a};
     ck(cudaLaunchKernel((const void*)kern, dim3(grid), dim3(t), args, dyn_smem, stream), "launch ff_step");
     // static rounds first (ff_step_body), then each block fetches dynamic tiles until it sees one past
-    // the end: the counter advances by the dynamic tiles + grid
-    tile_base += (uint64_t)(ntiles - ns * (int64_t)grid) + grid;
+    // the end: the counter advances by the dynamic tiles + grid (all-static launches do not touch it)
+    if (!all_static) tile_base += (uint64_t)(ntiles - ns * (int64_t)grid) + grid;
     ++launches;
     if (xworld > 1 && image) launch_exchange(m);  // (one rank: its image already is the sum)
   }

@@ -91,7 +91,7 @@ def _map_ipc(buf, group):
     return [t.data_ptr() for t in peers], rank, world, peers
 
 
-def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=60000.0, mapping="auto"):
+def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=1000.0, mapping="auto"):
     """Bind a peer-accessible image to `ctx` and turn on the library's image exchange: from now on
     every binning ff_step of every rank is followed, on its stream, by the sum of the images over all
     ranks (ff_set_exchange; no separate collective). Collective over `group` (default: the world);

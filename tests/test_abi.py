@@ -159,3 +159,15 @@ def test_uniform_factor_slots_and_sweep():
     slots = [int(v) for v in m.group(1).split(",")]
     assert [slots[i] for i in (0, 5, 10)] == [0, 0, 0]       # dV/dt = (...)/C: one shared slot
     assert all(v == -1 for i, v in enumerate(slots) if i not in (0, 5, 10))
+
+
+def test_multi_line_rhs_text_stays_in_its_comment():
+    """A right-hand side written over several lines (newlines are whitespace to the tokenizer) compiles:
+    the text echoed into the generated source's comments has its control characters blanked."""
+    s = systems.SystemDef("ml", ["x", "y"], ["-x\n  + 0.5*y", "x\r\n\t- y\n"], [])
+    src = FF.ff_emit_source(s)
+    head = src[:src.index("template <class V>")]
+    for ln in head.splitlines():
+        if "dx/dt" in ln or "dy/dt" in ln:
+            assert ln.lstrip().startswith("//")
+    assert FF.ff_compile_cubin(s)[:4] == b"\x7fELF"

@@ -67,3 +67,35 @@ def test_reference_arm_under_torchrun_prints_once():
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.strip().splitlines() if l.startswith("{")]
     assert len(lines) == 1 and json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_frozen_l_alg_matches_the_front_ends_plain_count():
+    """L_alg is frozen in bench.py; the front end's plain-formulation count of the same
+    RHS text must still agree (STN-GPe, HH ring), Lorenz within the one contraction the survey's probe
+    found (45 vs 44)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for name, (fma, mufu) in bench.L_ALG.items():
+        pf, pm, *_ = bench.op_counts(bench.make_system(name), -1)
+        assert pm == mufu, name
+        assert pf == fma or (name == "lorenz" and pf == fma + 1), (name, pf, fma)
+    assert bench.L_ALG["hh_ring3"][1] == 132 and bench.L_ALG["lorenz"] == (44, 0)
+
+
+def test_gpus_n_without_torchrun_fails_loudly_without_gpus():
+    """`bench.py --gpus 2` outside torchrun re-launches itself under torch.distributed.run -- after
+    checking that 2 GPUs are visible; here (none) it must exit non-zero with a message, not print a
+    1-rank line."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1",
+                          "--warmup", "1", "--config", "stn"], capture_output=True, text=True, timeout=600,
+                         cwd=ROOT, env=dict(os.environ, CUDA_VISIBLE_DEVICES=""))
+    assert out.returncode != 0
+    assert "needs 2 visible GPUs" in out.stderr
+    assert not [l for l in out.stdout.splitlines() if l.startswith("{")]
+
+
+def test_world_size_must_match_gpus():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1",
+                          "--warmup", "1", "--config", "stn"], capture_output=True, text=True, timeout=600,
+                         cwd=ROOT, env=dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0"))
+    assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr

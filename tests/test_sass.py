@@ -93,7 +93,9 @@ def test_front_end_op_counts():
     -> a - (a+b)X for the 12 gating equations)."""
     import bench
     assert bench.op_counts(systems.lorenz(), -1) == (45, 0, 0, 41, 0, 0)
-    assert bench.op_counts(systems.hh_ring(3), -1) == (813, 84, 36, 741, 84, 4)
+    # HH plain: 11 MUFU ops per neuron and evaluation (7 exponentials + 4 reciprocals) = 132 per
+    # particle-step (SURVEY.md:36); executed: exponentials of one rate argument shared (reading R25)
+    assert bench.op_counts(systems.hh_ring(3), -1) == (825, 132, 84, 741, 84, 4)
     # STN-GPe is MUFU-bound: its two sigmoids share one reciprocal, and in one of the four RK4 stages
     # that reciprocal runs on the FMA pipe (ff_rcpp)
     assert bench.op_counts(systems.stn_gpe(), -1) == (62, 16, 8, 73, 11, 4)
@@ -106,8 +108,28 @@ def test_pipe_balanced_roofline_work():
     import bench
     assert bench.balanced_work(45, 0, 0) == (45.0, 0, "fma")
     assert bench.balanced_work(813, 84, 36, 4) == (813.0, 0, "fma")
+    assert bench.balanced_work(825, 132, 84, 4) == (929.0, 8, "fma+xu")   # HH plain: MUFU-bound
     work, k, pipes = bench.balanced_work(62, 16, 8)
     assert (k, pipes) == (4, "fma+xu") and work == 128 * 12 / 16
     work, k, pipes = bench.balanced_work(62, 16, 8, 4)   # pairs, then one reciprocal on the FMA pipe
     assert (k, pipes) == (0, "fma+xu") and work == 128 * 11 / 16
     assert bench.balanced_work(10, 16, 0) == (128.0, 0, "xu")
+
+
+def test_bench_kernel_p4_loop(tmp_path, monkeypatch):
+    """The bench's headline kernel: ff_step_p4_t128 in its long-launch build (8 blocks/SM, <= 64
+    registers; the runtime's choice for Lorenz launches of >= 8 steps): the inner loop holds 2 RK4
+    steps of 4 particles -- two independent FFMA2 chains -- = 2 x 4 x 41 / 2 = 164 packed FP32
+    instructions, nothing unpacked, no spills."""
+    monkeypatch.setenv("FF_TUNE_MINB_P4", "8")
+    p = tmp_path / "lorenz_p4.cubin"
+    p.write_bytes(FF.ff_compile_cubin(systems.lorenz()))
+    loops = [c for c in inner_loops(str(p), "ff_step_p4_t128") if c["FFMA2"] >= 80]
+    assert loops, "no packed RK4 loop found"
+    main = min(loops, key=lambda c: sum(c.values()))
+    assert main["FFMA2"] + main["FMUL2"] + main["FADD2"] == 164
+    assert main["FFMA"] == 0 and main["FADD"] == 0 and main["FMUL"] == 0
+    assert main["LDL"] == 0 and main["STL"] == 0
+    res = subprocess.run(["cuobjdump", "-res-usage", str(p)], capture_output=True, text=True).stdout
+    m = re.search(r"Function ff_step_p4_t128:\s+REG:(\d+) STACK:(\d+)", res)
+    assert m and int(m.group(1)) <= 64 and int(m.group(2)) == 0
