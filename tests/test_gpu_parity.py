@@ -59,8 +59,10 @@ def test_ic_golden_values():
 # ----------------------------------------------------------------------------- integrator parity
 @pytest.mark.parametrize("ppt,tpb", LAUNCHES)
 def test_lorenz_r28_tier_a(ppt, tpb):
-    # Tier A horizons (profiles/r01_parity_probe.jsonl): forward 30 steps (max 1.4e-6), backward
-    # 10 steps (max 1.0e-6; backward Lorenz particles blow up, so errors grow fast).
+    # Tier A horizons: forward 30 steps, backward 10 steps -- set by the oracle-only proxy (FP32 vs
+    # FP64 oracle from the same ICs, tools/calibrate_tiers.py -> profiles/r02_tier_calibration.json:
+    # forward max 1.4e-6 at 30 steps; backward 8.9e-7 at 10 but 1.2e-5 at 20 steps -- backward Lorenz
+    # particles blow up, so rounding differences grow fast), not by the GPU itself.
     n = 20000 + 77  # several tiles and a ragged tail
     ctx = lorenz_ctx([n, n])
     ctx.set_launch(ppt, tpb)
@@ -196,6 +198,23 @@ def test_stn_forward_1000_backward_100():
     ctx.step(900, 0.01)
     wf = oracle_group(O.STN, [0, 0], [1, 1], 1, 0, 5000, p, 0.01, 1000)
     assert tier_a(ctx.read_state(gf), wf, [1.0, 1.0]) <= 1e-5
+
+
+def test_stn_backward_group_1000_steps_tier_b():
+    """configs[0]'s backward group over its full 1000 steps (SURVEY.md 8(c) Tier B: p99 <= 1e-4, max
+    <= 1e-2; the oracle-only proxy FP32 vs FP64 gives p99 1.6e-5, max 2.9e-3,
+    profiles/r02_tier_calibration.json), finite on both sides or on neither."""
+    p, s = stn_params()
+    ctx = FF.Context(s, [5000, 5000])
+    ctx.init_group([0, 0], [1, 1], 5000, 1, 0, seed=1)
+    gb = ctx.init_group([0, 0], [1, 1], 5000, -1, 1, seed=11)
+    ctx.step(1000, 0.01)
+    want = oracle_group(O.STN, [0, 0], [1, 1], 11, 0, 5000, p, -0.01, 1000)
+    got = ctx.read_state(gb)
+    same, both = finite_agreement(got, want)
+    assert same.all()
+    e = scaled_error(got[:, both], want[:, both], [1.0, 1.0]).max(axis=0)
+    assert np.percentile(e, 99) <= 1e-4 and e.max() <= 1e-2
 
 
 def test_stn_limit_cycle_tier_b():
@@ -364,9 +383,15 @@ def test_histogram_aggregation_regimes_exact(ppt, tpb):
     assert want[0, 100, 7] > n // 5
 
 
-def test_fused_pipeline_matches_oracle_up_to_edge_particles():
+@pytest.mark.parametrize("ppt,tpb", [(0, 0), (4, 128), (2, 256), (2, 128), (1, 128)])
+def test_fused_pipeline_matches_oracle_up_to_edge_particles(ppt, tpb):
+    """Integrate + bin in one launch vs the oracle's integration and binning, in every launch
+    variant: the library default for 30 k particles (one particle per thread), the bench's 4-per-
+    thread kernel, and packed pairs in both block sizes."""
     n = 30000
     ctx = lorenz_ctx([n])
+    if ppt:
+        ctx.set_launch(ppt, tpb)
     g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=2)
     M = views.lorenz_camera()
     img = ctx.project([0, 1, 2], M, 512, 512, 1)
