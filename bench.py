@@ -31,6 +31,7 @@ METRIC = "particle-steps/s per B200 and per box (Lorenz RK4, 15-D neuron); % FP3
 N_SM = 148
 FMA_LANES = 128   # FP32 lanes per SM (FFMA2 does not raise it: profiles/r01_ubench_pipes.txt)
 XU_LANES = 16     # MUFU results per clock per SM (same microbenchmark)
+RED_PEAK = 2.21e11    # L2 reductions / s on 4 M distinct words (tools/ubench/pipes.cu, profiles/r02_ubench_pipes.txt)
 
 # Algorithmic work per particle-step: FP32 FMA-pipe lane-ops of the plain
 # formulation with a*b+c contracted (Lorenz: 4 RHS x 6 + 3 dims x 7 RK4 combination = 45), MUFU ops
@@ -594,11 +595,17 @@ def main():
         "hbm": (r["n_local"] * 8 * dim / kern_s, peaks.get("hbm_gbs", 6549.1) * 1e9, "GB/s",
                 "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)", 8 * dim / r["S"]),
     }
+    if r["image_sum"] > 0 and world == 1:
+        # histogram increments: one per binned particle into the L2-resident image (an upper bound on
+        # the REDs issued: the warp / block aggregation can only merge them); peak = the measured L2
+        # reduction rate on 1-4 M distinct words (profiles/r02_ubench_pipes.txt: 2.14-2.21e11/s)
+        cands["l2_red"] = (r["image_sum"] / kern_s, RED_PEAK, "increments/s (1e9)",
+                           "measured REDG rate, 4 M distinct words (profiles/r02_ubench_pipes.txt)", 1.0 / r["S"])
     fracs = {k: v[0] / v[1] for k, v in cands.items()}
     pipe = max(fracs, key=fracs.get)
     ach, peak, unit, src, per_unit = cands[pipe]
-    scale = 1e9 if pipe == "hbm" else 1e12
-    roof = {"bound": "hbm" if pipe == "hbm" else "alu", "pipe": pipe if pipe == "hbm" else alu_pipes,
+    scale = 1e12 if pipe == "alu" else 1e9
+    roof = {"bound": pipe if pipe != "alu" else "alu", "pipe": alu_pipes if pipe == "alu" else pipe,
             "unit": unit, "achieved": ach / scale,
             "peak": peak / scale, "frac": ach / peak, "peak_source": src,
             "alg_per_particle_step": per_unit,

@@ -11,7 +11,8 @@ KEYS = [
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe % (active)"),
     ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA-pipe inst % (active)"),
-    ("sm__pipe_xu_cycles_active.avg.pct_of_peak_sustained_active", "XU pipe % (active)"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) inst % (active)"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU inst % (active)"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
     ("launch__registers_per_thread", "registers/thread"),
@@ -19,7 +20,7 @@ KEYS = [
     ("launch__block_size", "block"),
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
     ("lts__t_sectors_srcunit_tex_op_red.sum", "L2 RED sectors"),
     ("smsp__inst_executed.sum", "warp instructions"),
 ]

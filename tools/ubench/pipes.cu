@@ -127,7 +127,9 @@ __global__ void k_rcp(const float* __restrict__ in, float* out, long long* cyc) 
 #pragma unroll 2
   for (int it = 0; it < ITERS / 4; ++it) {
 #pragma unroll
-    for (int i = 0; i < NACC; ++i) a[i] = rcp(a[i]);
+    // rcp(rcp(a)) = a let ptxas drop the whole chain (r01 printed ~4e6 lane-ops/clk); one FFMA per
+    // reciprocal keeps it a chain (the FMA pipe has 8x the MUFU's throughput, so MUFU still binds)
+    for (int i = 0; i < NACC; ++i) a[i] = rcp(fmaf(a[i], 0.5f, 1.0f));
   }
   __syncthreads();
   long long t1 = clock64();
