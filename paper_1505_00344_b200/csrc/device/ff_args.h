@@ -57,6 +57,7 @@ struct FFStepArgs {
   float s0, s1;         // 2-D scales W/(hi0-lo0), H/(hi1-lo1), computed by the host in float
   float fW, fH, hW, hH; // (float)W, (float)H, W * 0.5f, H * 0.5f (exact; host-computed)
   int ax_id;            // 1: axes[j] == j for every projected axis (no per-particle axis selection)
+  float one;            // 1.0f, at run time (ff_exact.cuh: exact packed sums as fma(a, one, b))
   int n_groups;
   // device-side reset (NEXT row 1): 0 off, else bit 1 = bounds, bit 2 = age
   int reset;

@@ -1372,13 +1372,15 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   // (small systems run the 256-thread packed kernel for launches of >= 50 steps: 6 blocks / <= 40
   // registers, tools/gpu_run73.sh)
   int minb_p2 = dim <= 4 ? 6 : (dim <= 8 ? 2 : 1);
-  // 128-thread packed kernel, small systems: launches of a few steps want full occupancy (16 blocks
-  // = 64 warps/SM, <= 32 registers) to hide the state loads and the histogram reductions; launches
-  // of many steps are FMA-pipe bound and run best with 12 blocks / <= 40 registers (measured on
-  // B200, Lorenz 8.4 M, tools/gpu_run66.sh / gpu_run67.sh: S = 100 7.91 -> 8.06e11, S = 1000
-  // 8.32 -> 8.46e11, S = 10 +1%; S = 1, 2, 4 lose 9%, 5%, 3%). tests/test_sass.py checks that the
-  // inner loops do not spill.
-  int minb_p2_t128 = dim <= 4 ? (long_launch ? 12 : 16) : (dim <= 8 ? 4 : 2);
+  // 128-thread packed kernel, small systems: 12 blocks / <= 40 registers. Launches of many steps are
+  // FMA-pipe bound and run best there (measured on B200, Lorenz 8.4 M, tools/gpu_run66.sh /
+  // gpu_run67.sh: S = 100 7.91 -> 8.06e11, S = 1000 8.32 -> 8.46e11, S = 10 +1% over 16 blocks);
+  // round 1 kept full occupancy (16 blocks, <= 32 registers) for launches of a few steps, but with
+  // the packed 3-D binning and the reset rule of the bench workload the 32-register build spills and
+  // 12 blocks win there too (S = 1 / 2 / 4 / 7: 93.1 -> 88.7, 120 -> 117, 136 -> 131, 164 -> 162 us,
+  // tools/r02/run13.sh). tests/test_sass.py checks that the inner loops do not spill.
+  int minb_p2_t128 = dim <= 4 ? 12 : (dim <= 8 ? 4 : 2);
+  (void)long_launch;
   if (const char* e = std::getenv("FF_TUNE_MINB_P2_T128")) minb_p2_t128 = std::atoi(e);
   // 4 particles per thread, 128-thread blocks: 1-4-step launches without an image (memory-bound,
   // Lorenz 76 registers at 6 blocks/SM); long launches of FMA-bound small systems at 8 blocks /
@@ -1403,6 +1405,9 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   int prefetch = 0;
   if (const char* e = std::getenv("FF_TUNE_PREFETCH")) prefetch = std::atoi(e);
   pre << "#define FF_PREFETCH " << prefetch << "\n";
+  int packed_bin = 1;
+  if (const char* e = std::getenv("FF_TUNE_PACKED_BIN")) packed_bin = std::atoi(e);
+  pre << "#define FF_PACKED_BIN " << packed_bin << "\n";
 
   std::string tmpl(kDeviceTemplate);
   const std::string marker = "#include_generated_rhs";

@@ -21,7 +21,7 @@
 static_assert(sizeof(FFGroup) == 120, "FFGroup layout");
 static_assert(FF_MAX_SCALED_ == FF_MAX_SCALED, "scaled-component table size");
 static_assert(FF_MAX_DERIVED_ == FF_MAX_DERIVED, "derived-value table size");
-static_assert(offsetof(FFStepArgs, g) == 768, "FFStepArgs layout");
+static_assert(offsetof(FFStepArgs, g) == 768, "FFStepArgs layout");  // (one: in the padding before g)
 static_assert(FF_MAX_PEERS_ == FF_MAX_PEERS, "peer table size");
 static_assert(FF_MAX_DIM_ == FF_MAX_DIM, "bounds table size");
 static_assert(FF_MAX_GROUPS_ == FF_MAX_GROUPS, "group table size");
@@ -343,6 +343,7 @@ struct ff_ctx {
     a.fH = (float)H;
     a.hW = (float)W * 0.5f;
     a.hH = (float)H * 0.5f;
+    a.one = 1.0f;
     a.ax_id = 1;
     for (int j = 0; j < proj; ++j) a.ax_id &= axes[j] == j;
     a.n_groups = (int)groups.size();

@@ -1,5 +1,6 @@
-// Bit-for-bit check of ff_div2 (csrc/device/ff_exact.cuh: two quotients sharing one reciprocal, the
-// 3-D projection's c_x / c_w, c_y / c_w) against div.rn.f32 (tests/test_gpu_division.py).
+// Bit-for-bit check of ff_div2 and ff_div2_pair (csrc/device/ff_exact.cuh: two quotients sharing one
+// reciprocal, the 3-D projection's c_x / c_w, c_y / c_w; the pair form through FFMA2 / FMUL2) against
+// div.rn.f32 (tests/test_gpu_division.py).
 // Operands come from a counter-based hash, per mode:
 //   0  random bit patterns inside the fast box (d in [2^-60, 2^60], |n| in [2^-40, 2^64))
 //   1  random bit patterns over all floats (inf, NaN, zeros, denormals included; d > 0 forced)
@@ -46,6 +47,7 @@ __device__ void operands(int mode, uint64_t i, uint64_t seed, float& nx, float& 
 __device__ __forceinline__ bool same(float x, float y) {   // bitwise, any NaN equal to any NaN
   return __float_as_uint(x) == __float_as_uint(y) || (x != x && y != y);
 }
+// fast[0]: scalar fast-path operands, fast[1]: pairs that took the packed fast path
 __global__ void k_check(int mode, uint64_t n, uint64_t seed, unsigned long long* bad, unsigned long long* fast,
                         float* first) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -60,19 +62,32 @@ __global__ void k_check(int mode, uint64_t n, uint64_t seed, unsigned long long*
     if (!same(qx, rx) || !same(qy, ry)) {
       if (atomicAdd(bad, 1ull) == 0ull) { first[0] = nx; first[1] = ny; first[2] = d; }
     }
+    // the packed pair (ff_div2_pair): lane 0 = these operands, lane 1 = those of index i + n
+    float nx1, ny1, d1;
+    operands(mode, i + n, seed, nx1, ny1, d1);
+    if (!(d1 > 0.0f)) continue;
+    float2 px, py;
+    if (ff_div2_pair(make_float2(nx, nx1), make_float2(ny, ny1), make_float2(d, d1), make_float2(1.0f, 1.0f), px, py)) {
+      atomicAdd(fast + 1, 1ull);
+      if (!same(px.x, rx) || !same(py.x, ry) || !same(px.y, ieee_div(nx1, d1)) || !same(py.y, ieee_div(ny1, d1))) {
+        if (atomicAdd(bad, 1ull) == 0ull) { first[0] = nx1; first[1] = ny1; first[2] = d1; }
+      }
+    }
   }
 }
 extern "C" int div_check(int mode, unsigned long long n, unsigned long long seed, unsigned long long* out) {
   unsigned long long* dv;
   float* f;
-  if (cudaMalloc(&dv, 2 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  if (cudaMalloc(&dv, 3 * sizeof(unsigned long long)) != cudaSuccess) return 1;
   if (cudaMalloc(&f, 3 * sizeof(float)) != cudaSuccess) return 1;
-  cudaMemset(dv, 0, 2 * sizeof(unsigned long long));
+  cudaMemset(dv, 0, 3 * sizeof(unsigned long long));
   cudaMemset(f, 0, 3 * sizeof(float));
   k_check<<<148 * 8, 256>>>(mode, n, seed, dv, dv + 1, f);
   if (cudaDeviceSynchronize() != cudaSuccess) return 2;
   float hf[3];
-  cudaMemcpy(out, dv, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  unsigned long long cnt[3];
+  cudaMemcpy(cnt, dv, sizeof cnt, cudaMemcpyDeviceToHost);
+  out[0] = cnt[0]; out[1] = cnt[1]; out[5] = cnt[2];
   cudaMemcpy(hf, f, sizeof hf, cudaMemcpyDeviceToHost);
   for (int k = 0; k < 3; ++k) { uint32_t u; memcpy(&u, &hf[k], 4); out[2 + k] = u; }
   cudaFree(dv);
