@@ -1225,7 +1225,7 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   constexpr double kExp2pCost = 12.0;
   // the same for a pair reciprocal on the FMA pipe (ff_rcpp, 7 ops): measured on the STN-GPe
   // bifurcation with pairs and no exponential moved, R = 0..4 stages -> 3.58, 3.70, 3.44, 3.18,
-  // 2.98e11 (tools/gpu_run62.sh), which a cost of 12 ranks; ties go to fewer executed ops
+  // 2.98e11 (tools/r01/gpu_run62.sh), which a cost of 12 ranks; ties go to fewer executed ops
   constexpr double kRcppCost = 12.0;
   int R = 0;   // stages (of 4) whose pair reciprocals run on the FMA pipe (with k_lo exponentials)
   const int n_pair_eval = (int)pairs.size() / 2;
@@ -1364,16 +1364,16 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   for (int i = 0; i < s.dim; ++i) rhs << (i ? ", " : "") << slot[i];
   rhs << "};\n";
   const int dim = s.dim;
-  // RK4 steps per unrolled loop iteration; small systems, measured on B200 (tools/gpu_run70.sh):
+  // RK4 steps per unrolled loop iteration; small systems, measured on B200 (tools/r01/gpu_run70.sh):
   // FMA-bound Lorenz 2 > 3 > 4 (S = 100: 8.13 / 8.09 / 8.07e11), MUFU-bound STN-GPe 8 > 4 (3.74 /
   // 3.69e11: more independent MUFU work in flight per warp)
   int unroll = dim <= 4 ? (n_mufu > 0 ? 8 : 2) : (dim <= 8 ? 2 : 1);
   int minb_p1 = dim <= 4 ? 4 : (dim <= 8 ? 3 : (dim <= 16 ? 2 : 1));
   // (small systems run the 256-thread packed kernel for launches of >= 50 steps: 6 blocks / <= 40
-  // registers, tools/gpu_run73.sh)
+  // registers, tools/r01/gpu_run73.sh)
   int minb_p2 = dim <= 4 ? 6 : (dim <= 8 ? 2 : 1);
   // 128-thread packed kernel, small systems: 12 blocks / <= 40 registers. Launches of many steps are
-  // FMA-pipe bound and run best there (measured on B200, Lorenz 8.4 M, tools/gpu_run66.sh /
+  // FMA-pipe bound and run best there (measured on B200, Lorenz 8.4 M, tools/r01/gpu_run66.sh /
   // gpu_run67.sh: S = 100 7.91 -> 8.06e11, S = 1000 8.32 -> 8.46e11, S = 10 +1% over 16 blocks);
   // round 1 kept full occupancy (16 blocks, <= 32 registers) for launches of a few steps, but with
   // the packed 3-D binning and the reset rule of the bench workload the 32-register build spills and
@@ -1384,7 +1384,7 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   if (const char* e = std::getenv("FF_TUNE_MINB_P2_T128")) minb_p2_t128 = std::atoi(e);
   // 4 particles per thread, 128-thread blocks: 1-4-step launches without an image (memory-bound,
   // Lorenz 76 registers at 6 blocks/SM); long launches of FMA-bound small systems at 8 blocks /
-  // <= 64 registers (two FFMA2 chains per thread: Lorenz S = 100 8.22 -> 8.41e11, tools/gpu_run76.sh)
+  // <= 64 registers (two FFMA2 chains per thread: Lorenz S = 100 8.22 -> 8.41e11, tools/r01/gpu_run76.sh)
   int minb_p4 = dim <= 4 ? (long_launch ? 8 : 6) : (dim <= 8 ? 2 : 1);
   if (const char* e = std::getenv("FF_TUNE_MINB_P4")) minb_p4 = std::atoi(e);
   // tuning knobs for experiments (not part of the ABI): FF_TUNE_MINB_P2, FF_TUNE_UNROLL
@@ -1402,9 +1402,6 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   pre << "#define FF_MINB_P4 " << minb_p4 << "\n";
   pre << "#define FF_SWEEP " << sweep_param << "\n";
   pre << "#define FF_KSEL " << kernel_select << "\n";
-  int prefetch = 0;
-  if (const char* e = std::getenv("FF_TUNE_PREFETCH")) prefetch = std::atoi(e);
-  pre << "#define FF_PREFETCH " << prefetch << "\n";
   int packed_bin = 1;
   if (const char* e = std::getenv("FF_TUNE_PACKED_BIN")) packed_bin = std::atoi(e);
   pre << "#define FF_PACKED_BIN " << packed_bin << "\n";

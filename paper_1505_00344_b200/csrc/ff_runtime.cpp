@@ -278,7 +278,7 @@ struct ff_ctx {
     const bool wide = n_steps >= 50 && next_slot >= 4 * 512 * (int64_t)nsm;
     // FMA-bound small systems (no MUFU op): long launches run 4 particles per thread (two independent
     // FFMA2 chains, 8 blocks / <= 64 registers): Lorenz S = 10 / 100 / 1000 +4 / +2.3 / +2.8%; a
-    // MUFU-bound one (STN-GPe) loses 6% there (tools/gpu_run76.sh)
+    // MUFU-bound one (STN-GPe) loses 6% there (tools/r01/gpu_run76.sh)
     if (!ppt && !tpb && sys.dim <= 4 && n_steps >= 8 && next_slot >= 4 * 512 * (int64_t)nsm &&
         uprogram(sweep_param, true).mufu_per_step == 0) {
       ppt_out = 4;
@@ -415,15 +415,15 @@ struct ff_ctx {
     if (grid_limit > 0 && grid_limit < resident) resident = grid_limit;
     const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
     // static tile rounds for 1-2-step launches (ff_step_body): all but the last round of tiles
-    int64_t ns = (n_steps <= 2 && sys.dim <= 8 && ntiles / grid >= 2) ? ntiles / grid - 1 : 0;
-    static const int all_static_max = std::getenv("FF_TUNE_STATIC_ALL") ? std::atoi(std::getenv("FF_TUNE_STATIC_ALL")) : 0;
-    const bool all_static = sys.dim <= 8 && n_steps <= all_static_max;
-    a.static_rounds = all_static ? -1 : (int)ns;
+    // (all-static tile rounds -- no counter, no per-tile barrier -- measured slower at S = 1: 99 vs
+    // 93 us, tools/r02/run04.sh; so is a register prefetch of the next tile's state: 107 us)
+    const int64_t ns = (n_steps <= 2 && sys.dim <= 8 && ntiles / grid >= 2) ? ntiles / grid - 1 : 0;
+    a.static_rounds = (int)ns;
     void* args[] = {&a};
     ck(cudaLaunchKernel((const void*)kern, dim3(grid), dim3(t), args, dyn_smem, stream), "launch ff_step");
     // static rounds first (ff_step_body), then each block fetches dynamic tiles until it sees one past
-    // the end: the counter advances by the dynamic tiles + grid (all-static launches do not touch it)
-    if (!all_static) tile_base += (uint64_t)(ntiles - ns * (int64_t)grid) + grid;
+    // the end: the counter advances by the dynamic tiles + grid
+    tile_base += (uint64_t)(ntiles - ns * (int64_t)grid) + grid;
     ++launches;
     if (xworld > 1 && image) launch_exchange(m);  // (one rank: its image already is the sum)
   }
