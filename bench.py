@@ -163,20 +163,24 @@ def setup(args, w, rank, world):
     if w.get("prerun"):
         ctx.step(w["prerun"], w["dt"])
     axes, view = projection(w)
-    fused = not args.no_image and (args.exchange == "fused" or (args.exchange == "auto" and world > 1))
+    fused = not args.no_image and (args.exchange in ("fused", "nvls") or (args.exchange == "auto" and world > 1))
     img = None
     if fused:   # the image sum over ranks is done by the library after each launch, no NCCL call
         from paper_1505_00344_b200 import dist as ffdist
         try:
-            img = ffdist.bind_exchanged_image(ctx, axes, view, w["W"], w["H"], w["C"])
-            if args.exchange == "auto":
+            if args.exchange == "nvls":   # NVSwitch multicast sum pass (multimem), torch symmetric memory
+                img = ffdist.bind_exchanged_image(ctx, axes, view, w["W"], w["H"], w["C"], mapping="symmetric",
+                                                  multicast=True)
+            else:
+                img = ffdist.bind_exchanged_image(ctx, axes, view, w["W"], w["H"], w["C"])
+            if args.exchange in ("auto", "nvls"):
                 ok, why = validate_exchange(ctx, img, w)
                 if not ok:
                     raise RuntimeError(why)
         except Exception as e:   # auto: fall back to the NCCL all-reduce, say why in the line
             if args.exchange == "fused":
                 raise
-            args.exchange_note = f"library exchange unavailable ({str(e)[:160]}); NCCL all-reduce used"
+            args.exchange_note = f"library exchange ({args.exchange}) unavailable ({str(e)[:160]}); NCCL all-reduce used"
             ctx.set_exchange(0, 0)
             fused, img = False, None
     if img is None:
@@ -496,11 +500,12 @@ def main():
                     help="L2 flush between timed frames (default: read 256 MiB; 'none' only for experiments)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-reset", action="store_true", help="(experiments) leave the workload's reset rule off")
-    ap.add_argument("--exchange", default="nccl", choices=["auto", "nccl", "fused"],
+    ap.add_argument("--exchange", default="nccl", choices=["auto", "nccl", "fused", "nvls"],
                     help="per-frame image sum over ranks (N > 1): an NCCL all-reduce (default), or the "
                          "library's exchange over peer memory after each launch (ff_set_exchange; 'auto' "
                          "validates it once and falls back to NCCL) -- not the default until it has run "
-                         "across physical GPUs")
+                         "across physical GPUs; 'nvls' = the library exchange with its sum pass through "
+                         "NVSwitch multicast (multimem), validated likewise")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = WORKLOADS[args.config]
@@ -560,9 +565,11 @@ def main():
     r = run_ours(args, w, rank, world, device)
     if world > 1:
         config["parallelism"] = f"particles sharded over {world} GPU(s), " + (
-            "image sum by the library's exchange kernel over NVLink peer memory after each launch"
+            ("image sum by the library's exchange kernel (NVLS multimem sum pass) after each launch"
+             if args.exchange == "nvls" else
+             "image sum by the library's exchange kernel over NVLink peer memory after each launch")
             if r["fused"] else "NCCL image all-reduce per frame")
-        config["exchange"] = "library" if r["fused"] else "nccl"
+        config["exchange"] = ("library-nvls" if args.exchange == "nvls" else "library") if r["fused"] else "nccl"
         if getattr(args, "exchange_note", None):
             config["exchange_note"] = args.exchange_note
     if world > 1:

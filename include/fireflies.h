@@ -314,6 +314,18 @@ ff_status ff_sync(ff_ctx* ctx);
 ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* peer_images,
                           uint64_t* const* peer_signals, double timeout_ms);
 
+/* NVLS variant of the image exchange (NVSwitch multicast): after
+ * ff_set_exchange, give the multicast address under which every rank's bound image is mapped (a CUDA
+ * multicast object bound to each rank's image buffer, same layout; e.g. torch symmetric memory's
+ * multicast_ptr). The exchange keeps its two barriers; its sum pass then uses multimem.ld_reduce
+ * (the switch adds the ranks' words) and multimem.st (the sum lands in every rank's image), one word
+ * per instruction, so each word of this rank's slice crosses NVLink once in each direction. Same
+ * result, bit-exact. Needs a multicast-capable NVSwitch system with >= 2 GPUs (on a single GPU the
+ * driver refuses multicast objects). mc_image = NULL returns to peer loads / stores; ff_set_exchange
+ * and rebinding the image clear it. Errors: FF_ERR_STATE (no exchange set), FF_ERR_INVALID_ARG
+ * (misaligned). */
+ff_status ff_set_exchange_multicast(ff_ctx* ctx, uint32_t* mc_image);
+
 /* Upper bound on the blocks of every step and exchange launch (0 = the default: every resident block
  * for a step, 2 per SM for an exchange). For several ranks sharing one GPU (their exchanges must run
  * concurrently), and for tuning. Errors: FF_ERR_INVALID_ARG. */

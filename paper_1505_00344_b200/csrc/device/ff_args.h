@@ -97,6 +97,7 @@ struct FFXchgArgs {
   ff_u64 seq;                   // exchanges before this one: barrier values 2 seq + 1, 2 seq + 2
   ff_u64 timeout_ns;            // bound on every wait (a missing peer cannot hang the GPU)
   int rank, world;
+  ff_u32* mc;                   // NVLS multicast address of the images (same layout) or null
 };
 
 // Lifted-parameter readback (ff_read_lifted): the swept value of particles [local, local + count) of

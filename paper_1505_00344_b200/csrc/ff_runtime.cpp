@@ -125,6 +125,7 @@ struct ff_ctx {
   uint64_t* xsig[FF_MAX_PEERS] = {};
   uint64_t xbar = 0, xseq = 0, xtimeout_ns = 0;
   bool xused = false;
+  uint32_t* xmc = nullptr;   // NVLS multicast address of the images (ff_set_exchange_multicast)
 
   ~ff_ctx() {
     for (auto& m : modules) {
@@ -443,6 +444,7 @@ struct ff_ctx {
     x.timeout_ns = xtimeout_ns;
     x.rank = xrank;
     x.world = xworld;
+    x.mc = xmc;
     // 2 blocks of 256 threads per SM (fewer if ff_set_grid_limit says so): enough loads in flight
     unsigned grid = (unsigned)(2 * nsm);
     if (grid_limit > 0 && (unsigned)grid_limit < grid) grid = (unsigned)grid_limit;
@@ -805,6 +807,7 @@ ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view
     ctx->colour_img = nullptr;
     ctx->proj = 0;
     ctx->xworld = 0;
+    ctx->xmc = nullptr;
     return FF_OK;
   }
   need(axes && view, FF_ERR_INVALID_ARG, "axes / view is NULL");
@@ -837,6 +840,7 @@ ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view
   ctx->C = C;
   ctx->image = image;
   ctx->xworld = 0;  // (re)binding an image ends an exchange (ff_set_exchange again)
+  ctx->xmc = nullptr;
   if (!ctx->groups.empty()) ctx->launch_step(0, 0.0f);
   FF_CATCH
 }
@@ -1015,6 +1019,8 @@ ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* pee
   need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
   if (world == 0) {
     ctx->xworld = 0;
+    ctx->xmc = nullptr;
+    ctx->xmc = nullptr;
     return FF_OK;
   }
   need(world >= 1 && world <= FF_MAX_PEERS && rank >= 0 && rank < world, FF_ERR_INVALID_ARG,
@@ -1055,6 +1061,16 @@ ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* pee
   ctx->xworld = world;
   ctx->xseq = 0;
   ctx->xtimeout_ns = (uint64_t)(timeout_ms * 1e6);
+  ctx->xmc = nullptr;
+  FF_CATCH
+}
+
+ff_status ff_set_exchange_multicast(ff_ctx* ctx, uint32_t* mc_image) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  need(mc_image == nullptr || ctx->xworld >= 1, FF_ERR_STATE, "set up the exchange with ff_set_exchange first");
+  need(((uintptr_t)mc_image & 15) == 0, FF_ERR_INVALID_ARG, "the multicast address must be 16-byte aligned");
+  ctx->xmc = mc_image;
   FF_CATCH
 }
 

@@ -91,12 +91,15 @@ def _map_ipc(buf, group):
     return [t.data_ptr() for t in peers], rank, world, peers
 
 
-def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=1000.0, mapping="auto"):
+def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=1000.0, mapping="auto",
+                         multicast=False):
     """Bind a peer-accessible image to `ctx` and turn on the library's image exchange: from now on
     every binning ff_step of every rank is followed, on its stream, by the sum of the images over all
     ranks (ff_set_exchange; no separate collective). Collective over `group` (default: the world);
     returns the bound image tensor [C][H][W] (int32, zeroed). mapping: "symmetric" (torch symmetric
-    memory), "ipc" (CUDA IPC handles), "auto" (symmetric, else IPC)."""
+    memory), "ipc" (CUDA IPC handles), "auto" (symmetric, else IPC). multicast=True additionally binds
+    the NVLS multicast mapping of the images (torch symmetric memory's multicast_ptr;
+    ff_set_exchange_multicast) and raises if the system offers none."""
     words, sig_off, total = exchange_layout(C_, H, W)
     if not dist.is_initialized() or dist.get_world_size(group) == 1:   # one rank: its own tables
         buf = torch.zeros(total, dtype=torch.int32, device=ctx.device)
@@ -133,5 +136,13 @@ def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=100
     dist.barrier(group)                                # every rank's signals are zero
     imgs, sigs = peer_tables(ptrs, C_, H, W)
     ctx.set_exchange(rank, world, imgs, sigs, timeout_ms)
+    if multicast:
+        mc = int(getattr(keep, "multicast_ptr", 0) or 0)
+        ok = torch.tensor([1 if mc else 0], dtype=torch.int32, device=ctx.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)   # all ranks or none
+        if not int(ok.item()):
+            ctx.set_exchange(0, 0)
+            raise RuntimeError("no NVLS multicast mapping for this group (symmetric memory multicast_ptr = 0)")
+        ctx.set_exchange_multicast(mc)
     ctx._symm = (buf, keep)                            # keep the mappings alive with the context
     return image

@@ -201,6 +201,11 @@ def ff_set_exchange(ctx, rank: int, world: int, peer_image_ptrs, peer_signal_ptr
     check(lib().ff_set_exchange(ctx, rank, world, imgs, sigs, timeout_ms))
 
 
+def ff_set_exchange_multicast(ctx, mc_image_ptr: int):
+    """NVLS multicast address of the exchanged images (0: peer loads / stores)."""
+    check(lib().ff_set_exchange_multicast(ctx, C.c_void_p(int(mc_image_ptr)) if mc_image_ptr else None))
+
+
 def ff_set_grid_limit(ctx, max_blocks: int):
     check(lib().ff_set_grid_limit(ctx, max_blocks))
 
@@ -335,6 +340,9 @@ class Context:
 
     def set_exchange(self, rank, world, peer_image_ptrs=(), peer_signal_ptrs=(), timeout_ms=60000.0):
         ff_set_exchange(self.ctx, rank, world, peer_image_ptrs, peer_signal_ptrs, timeout_ms)
+
+    def set_exchange_multicast(self, mc_image_ptr):
+        ff_set_exchange_multicast(self.ctx, mc_image_ptr)
 
     def set_grid_limit(self, max_blocks):
         ff_set_grid_limit(self.ctx, max_blocks)
