@@ -17,7 +17,15 @@
  *                          round trip, fixed points
  *   rhs_lorenz             pinned: PAPER.md:87-93 landmarks, analytic fixed points, rhs(1,1,1)
  *   rhs_hh                 pinned: textbook m,h,n steady states, rest 0 mV,
- *                          onset of repetitive firing ~6.25
+ *                          onset of repetitive firing ~6.25, the vtrap series
+ *                          branch (alpha_m(25) = 1, alpha_n(10) = 0.1, series vs expm1 within its
+ *                          truncation term, continuity at |u| = 0.1; reading R10); the synapse
+ *                          constants tau_r, tau_d, sigma, theta are unpublished
+ *                          -> "parity unpinned" for their values (reading R8)
+ *   rhs_funcs              pinned: closed forms at the origin and at 3 points where every term
+ *                          is non-zero (Python math, double)
+ *   reset / lifted values  pinned: an independent Python Philox4x32-10 golden
+ *                          (tests/golden/reset_golden.json), inclusive bounds, epochs, uniformity
  *   rhs_stn                pinned by special cases (w = 0 closed form, forward invariance of
  *                          (0,1)^2 per PAPER.md:40); the sigmoid constants themselves are
  *                          unpublished -> "parity unpinned" for their values (reading R6)

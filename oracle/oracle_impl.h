@@ -115,8 +115,9 @@ static void F(rhs_hh)(int dim, const REAL* x, const REAL* p, REAL* dx) {
 }
 
 /* Front-end coverage system (not from the paper; exercises every builtin function of the
- * expression grammar in include/fireflies.h). p = {a, b}. Pinned only by closed-form values at the
- * origin (tests/test_oracle_models.py) and the RK4 pins; otherwise "parity unpinned". */
+ * expression grammar in include/fireflies.h). p = {a, b}. Pinned by closed-form values at the
+ * origin and at three points where every term is non-zero (tests/test_oracle_models.py, Python's
+ * math module in double) and by the RK4 pins. */
 static void F(rhs_funcs)(int dim, const REAL* v, const REAL* p, REAL* dx) {
   (void)dim;
   const REAL x = v[0], y = v[1], z = v[2], a = p[0], b = p[1];
