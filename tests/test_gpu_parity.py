@@ -383,6 +383,37 @@ def test_histogram_aggregation_regimes_exact(ppt, tpb):
     assert want[0, 100, 7] > n // 5
 
 
+@pytest.mark.parametrize("ppt,tpb", [(1, 128), (2, 128), (4, 128), (2, 256)])
+def test_histogram_warp_regime_with_dropped_leading_lanes(ppt, tpb):
+    """Warps whose first lanes hold dropped particles (outside the window) while the others share one
+    pixel (the regime is judged on the first lane holding a particle), warps with no particle in view
+    at all, and warps in one pixel but for one stray -- bit-exact."""
+    n = 4096 * 8 + 5
+    ctx = lorenz_ctx([n])
+    ctx.set_launch(ppt, tpb)
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=1)
+    W, H = 64, 48
+    idx = np.arange(n)
+    x = np.zeros((3, n), np.float32)
+    x[0] = -10.0 + 20.0 * (idx % 977 % W + 0.5) / W        # default: scattered
+    x[1] = -30.0 + 60.0 * (idx % 331 % H + 0.5) / H
+    blk = (idx // 256) % 4
+    run = idx % 256
+    hot = blk == 0                                           # one pixel, the first 1..31 particles dropped
+    x[0, hot], x[1, hot] = -10.0 + 20.0 * 5.5 / W, -30.0 + 60.0 * 7.5 / H
+    x[0, hot & (run % 64 < 1 + (idx // 1024) % 31)] = 50.0
+    x[0, blk == 1] = 99.0                                    # nothing in view
+    stray = blk == 2                                         # one pixel but for one particle
+    x[0, stray], x[1, stray] = -10.0 + 20.0 * 40.5 / W, -30.0 + 60.0 * 3.5 / H
+    x[1, stray & (run % 64 == 63)] = 20.0
+    ctx.write_state(g, x)
+    view = [-10.0, 10.0, -30.0, 30.0]
+    ctx.project([0, 1], view, W, H, 1)
+    want = O.histogram(x, [0, 1], view, W, H, 1, 0)
+    assert np.array_equal(ctx.read_image(), want)
+    assert want[0, 7, 5] > n // 8
+
+
 @pytest.mark.parametrize("ppt,tpb", [(0, 0), (4, 128), (2, 256), (2, 128), (1, 128)])
 def test_fused_pipeline_matches_oracle_up_to_edge_particles(ppt, tpb):
     """Integrate + bin in one launch vs the oracle's integration and binning, in every launch
