@@ -32,6 +32,8 @@ N_SM = 148
 FMA_LANES = 128   # FP32 lanes per SM (FFMA2 does not raise it: profiles/r01_ubench_pipes.txt)
 XU_LANES = 16     # MUFU results per clock per SM (same microbenchmark)
 RED_PEAK = 2.21e11    # L2 reductions / s on 4 M distinct words (tools/ubench/pipes.cu, profiles/r02_ubench_pipes.txt)
+# stream + reductions in one kernel (tools/ubench/red_stream.cu, profiles/r02_ubench_red_stream.txt)
+L2_STREAM_BPS, L2_RED_RATE, L2_OVERLAP = 5.174e12, 1.64e11, 75.7 / (38.9 + 51.2)
 
 # Algorithmic work per particle-step: FP32 FMA-pipe lane-ops of the plain
 # formulation with a*b+c contracted (Lorenz: 4 RHS x 6 + 3 dims x 7 RK4 combination = 45), MUFU ops
@@ -608,10 +610,19 @@ def main():
         # reduction rate on 1-4 M distinct words (profiles/r02_ubench_pipes.txt: 2.14-2.21e11/s)
         cands["l2_red"] = (r["image_sum"] / kern_s, RED_PEAK, "increments/s (1e9)",
                            "measured REDG rate, 4 M distinct words (profiles/r02_ubench_pipes.txt)", 1.0 / r["S"])
+    if r["image_sum"] > 0 and world == 1 and r["S"] <= 4:
+        # short frames: the state stream and the random-pixel reductions share the L2 and barely overlap
+        # (tools/ubench/red_stream.cu: 39 us streaming 201 MB, 51 us for 8.4 M REDs, 75.7 us both in one
+        # kernel = 0.84 of the sum). Floor time = 0.84 x (bytes / 5.17 TB/s + increments / 1.64e11/s);
+        # reported as a throughput fraction (floor / launch time), "units" = launches.
+        t_floor = L2_OVERLAP * (r["n_local"] * 8 * dim / L2_STREAM_BPS + r["image_sum"] / L2_RED_RATE)
+        cands["l2_stream_red"] = (1.0 / kern_s, 1.0 / t_floor, "launches/s",
+                                  "measured floor of state stream + L2 reductions in one kernel "
+                                  "(profiles/r02_ubench_red_stream.txt)", None)
     fracs = {k: v[0] / v[1] for k, v in cands.items()}
     pipe = max(fracs, key=fracs.get)
     ach, peak, unit, src, per_unit = cands[pipe]
-    scale = 1e12 if pipe == "alu" else 1e9
+    scale = {"alu": 1e12, "l2_stream_red": 1.0}.get(pipe, 1e9)
     roof = {"bound": pipe if pipe != "alu" else "alu", "pipe": alu_pipes if pipe == "alu" else pipe,
             "unit": unit, "achieved": ach / scale,
             "peak": peak / scale, "frac": ach / peak, "peak_source": src,

@@ -241,3 +241,45 @@ def test_lifted_redraw_uses_a_second_philox_block_at_dim_4():
     got = ctx.read_state(g)[:, case["index"]]
     assert ["%08x" % v for v in got.view(np.uint32)] == case["bits"]
     assert "%08x" % ctx.read_lifted(g)[case["index"]:].view(np.uint32)[0] == case["lifted_bits"]
+
+
+@pytest.mark.parametrize("ppt,tpb", [(1, 128), (2, 128), (2, 256), (4, 128)])
+@pytest.mark.parametrize("density", [0.01, 0.2, 0.95])
+def test_redraws_bit_exact_at_any_reset_density(ppt, tpb, density):
+    """The redraw is warp-cooperative when a warp has few resets (jobs spread over the lanes, results
+    shuffled back) and per thread when it has many: both must give the oracle's bits. Particles of a
+    4-variable system with a Philox-swept lifted parameter (its redraw needs a second Philox block)
+    are poisoned with NaN at random at the given density and stepped with dt = 0 (nothing else
+    moves): every poisoned particle is redrawn exactly as the oracle's reset rule with its epoch
+    (state and lifted value), every other one keeps its bits."""
+    from paper_1505_00344_b200.systems import SystemDef
+    sysdef = SystemDef("lin4", ["a", "b", "c", "d"], ["k*a", "k*b", "k*c", "k*d"], [("k", 0.0, None, None)])
+    lo, hi, seed, sseed = [-1.0, 0.0, 2.0, -5.0], [1.0, 3.0, 2.5, 5.0], 31, 77
+    n = 20000 + 37
+    ctx = FF.Context(sysdef, [n])
+    ctx.set_launch(ppt, tpb)
+    g = ctx.init_group(lo, hi, n, 1, 0, seed=seed)
+    ctx.sweep_param(g, "k", 0.5, 1.5, 0, sseed)
+    ctx.set_reset(True)
+    rng = np.random.default_rng(int(density * 1000) + ppt)
+    prev_ep = np.zeros(n, np.uint32)
+    for _ in range(3):
+        before, lifted0 = ctx.read_state(g), ctx.read_lifted(g)
+        sel = rng.random(n) < density
+        st = before.copy()
+        st[:, sel] = np.nan
+        ctx.write_state(g, st)
+        ctx.step(1, 0.0)
+        ep, got, lifted = ctx.read_epochs(g), ctx.read_state(g), ctx.read_lifted(g)
+        assert np.array_equal(ep, prev_ep + sel.astype(np.uint32))
+        keep = ~sel
+        assert np.array_equal(got[:, keep].view(np.uint32), before[:, keep].view(np.uint32))
+        assert np.array_equal(lifted[keep].view(np.uint32), lifted0[keep].view(np.uint32))
+        for i in np.nonzero(sel)[0]:
+            col = np.full((4, 1), np.nan, np.float32)
+            sv = np.zeros(1, np.float32)
+            O.reset(col, None, None, 0.0, 0.0, np.zeros(1, np.float32), np.array([ep[i] - 1], np.uint32), lo, hi,
+                    seed, first_global=int(i), sweep=dict(vals=sv, lo=0.5, hi=1.5, mode=0, seed=sseed, n_group=n))
+            assert np.array_equal(got[:, i].view(np.uint32), col[:, 0].view(np.uint32)), i
+            assert sv.view(np.uint32)[0] == lifted[i:i + 1].view(np.uint32)[0], i
+        prev_ep = ep
