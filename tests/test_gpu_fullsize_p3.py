@@ -109,3 +109,29 @@ def test_lorenz3d_bench_frame_trajectories_and_resets():
             assert red.sum() > 0.9 * len(idx)           # (proxy at 100 steps: p99 5e-2, max 88)
             assert np.all(np.isfinite(got[:, kept]))
     ctx.close()
+
+
+@pytest.mark.slow
+def test_config5_lorenz_1B_frame_image_is_oracle_histogram():
+    """configs[4] on one B200 at its full 2^30 particles (12 GB of state), the bench's workload and
+    launch (`--config lorenz1b`: non-finite reset, 3-D image): after one fused frame the state is read
+    back in 2^26-particle chunks and the oracle's histogram of it, accumulated chunk by chunk, must
+    equal the GPU image bit for bit."""
+    import os as _os
+    try:   # the chunks need ~1 GB of host memory at a time; refuse on a small host rather than swap
+        if _os.sysconf("SC_PAGE_SIZE") * _os.sysconf("SC_AVPHYS_PAGES") < (8 << 30):
+            pytest.skip("needs >= 8 GB of free host memory")
+    except (ValueError, OSError):
+        pass
+    w, ctx, gids, img = frame("lorenz1b", 100)
+    got = ctx.read_image()
+    axes, view = bench.projection(w)
+    want = np.zeros((w["C"], w["H"], w["W"]), np.uint32)
+    (n, _, colour, _), g = w["groups"][0], gids[0]
+    chunk = 1 << 26
+    for first in range(0, n, chunk):
+        O.histogram(ctx.read_state(g, first, min(chunk, n - first)), axes, view, w["W"], w["H"], w["C"], colour,
+                    image=want)
+    assert np.array_equal(got, want), f"sums {int(got.sum())} vs {int(want.sum())}"
+    assert int(want.astype(np.int64).sum()) > n // 4
+    ctx.close()
