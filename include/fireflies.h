@@ -194,7 +194,14 @@ ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view
  * (dt may be negative), then, if an image is bound, bin every particle once
  * (fused). One kernel launch; async. n_steps >= 0 (0 = bin only).
  * The first launch of a kernel variant compiles it (NVRTC, ~0.5 s; cached per process).
- * Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE (no groups), FF_ERR_COMPILE, FF_ERR_CUDA. */
+ * CUDA-graph capture (replaying a recorded frame, PAPER.md:242's main loop): if the
+ * bound stream is capturing, the launch is recorded with its current parameters, dt, camera and
+ * groups, preceded by a reset of the library's tile counter (from then on every launch of this
+ * context resets it: replays and later launches agree). The kernel must already be compiled (run
+ * the same launch once first), and the age rule (t_max) and the image exchange cannot be captured.
+ * ff_launch_count counts captures, not replays.
+ * Errors: FF_ERR_INVALID_ARG, FF_ERR_STATE (no groups; capture restrictions), FF_ERR_COMPILE,
+ * FF_ERR_CUDA. */
 ff_status ff_step(ff_ctx* ctx, int64_t n_steps, float dt);
 
 /* Device-side reset (trajectories that leave the region, or have not been reset for

@@ -126,6 +126,7 @@ struct ff_ctx {
   uint64_t xbar = 0, xseq = 0, xtimeout_ns = 0;
   bool xused = false;
   uint32_t* xmc = nullptr;   // NVLS multicast address of the images (ff_set_exchange_multicast)
+  bool captured = false;     // a launch was captured into a CUDA graph: reset the tile counter per launch
 
   ~ff_ctx() {
     for (auto& m : modules) {
@@ -320,6 +321,22 @@ struct ff_ctx {
     default_launch(p, t, n_steps);
     const int si = step_index(p, t);
     Module& m = module(sweep_param);
+    // CUDA-graph capture of frames: a captured launch replays with the arguments it
+    // was captured with, so it must not depend on host bookkeeping that advances per launch
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    ck(cudaStreamIsCapturing(stream, &cs), "cudaStreamIsCapturing");
+    const bool capturing = cs == cudaStreamCaptureStatusActive;
+    if (capturing) {
+      if (reset & 2) throw ff::Error(FF_ERR_STATE, "graph capture: the age rule (t_max) needs the launch's time");
+      if (xworld > 1) throw ff::Error(FF_ERR_STATE, "graph capture: an exchanging context cannot be captured");
+      captured = true;
+    }
+    if (captured) {
+      // the tile counter restarts at 0 before every launch (a memset node in a graph), so replays and
+      // the launches issued after them agree on it
+      ck(cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned long long), stream), "cudaMemsetAsync tile counter");
+      tile_base = 0;
+    }
     FFStepArgs a;
     std::memset(&a, 0, sizeof a);
     a.state = state;
@@ -403,6 +420,9 @@ struct ff_ctx {
     const size_t dyn_smem = colour ? 3 * 1024 * sizeof(uint32_t) : 0;
     const int kid = si + (colour ? kNumStep : 0);
     const int var = variant_for(bal, kid, n_steps);
+    if (capturing && !m.step[var][kid])
+      throw ff::Error(FF_ERR_STATE, "graph capture: this launch's kernel is not compiled yet -- run the frame once "
+                                    "before capturing it");
     const cudaKernel_t kern = step_kernel(m, sweep_param, kid, var);
     int occ = m.occ[var][kid];
     if (colour) {

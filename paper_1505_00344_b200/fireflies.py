@@ -287,6 +287,22 @@ class Context:
     def step(self, n_steps, dt):
         ff_step(self.ctx, n_steps, dt)
 
+    def capture(self, frame):
+        """Record `frame()` -- e.g. `lambda: (img.zero_(), ctx.step(S, dt))` -- into a CUDA graph and
+        return the torch.cuda.CUDAGraph; `g.replay()` runs the frame again on torch's current stream
+        (SURVEY.md A8). Run the frame once before capturing it (its kernels compile at first use)."""
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(self.stream)
+        with torch.cuda.graph(g, stream=side):
+            ff_set_stream(self.ctx, side.cuda_stream)
+            try:
+                frame()
+            finally:
+                ff_set_stream(self.ctx, self.stream.cuda_stream)
+        return g
+
     def set_reset(self, enable=True, lo=None, hi=None, t_max=0.0):
         ff_set_reset(self.ctx, enable, lo, hi, t_max)
 
