@@ -1367,7 +1367,9 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   // RK4 steps per unrolled loop iteration; small systems, measured on B200 (tools/r01/gpu_run70.sh):
   // FMA-bound Lorenz 2 > 3 > 4 (S = 100: 8.13 / 8.09 / 8.07e11), MUFU-bound STN-GPe 8 > 4 (3.74 /
   // 3.69e11: more independent MUFU work in flight per warp)
-  int unroll = dim <= 4 ? (n_mufu > 0 ? 8 : 2) : (dim <= 8 ? 2 : 1);
+  // (HH ring, 15 variables: 2 steps per iteration 2445 -> 2391 us per 100-step frame, 3: 2627 us,
+  // tools/r02/run29.sh)
+  int unroll = dim <= 4 ? (n_mufu > 0 ? 8 : 2) : (dim <= 16 ? 2 : 1);
   int minb_p1 = dim <= 4 ? 4 : (dim <= 8 ? 3 : (dim <= 16 ? 2 : 1));
   // (small systems run the 256-thread packed kernel for launches of >= 50 steps: 6 blocks / <= 40
   // registers, tools/r01/gpu_run73.sh)

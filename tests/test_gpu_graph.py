@@ -52,7 +52,8 @@ def test_replayed_frames_equal_ordinary_frames(S):
         assert np.array_equal(a.read_state(x).view(np.uint32), b.read_state(y).view(np.uint32))
         assert np.array_equal(a.read_epochs(x), b.read_epochs(y))
     assert np.array_equal(a.read_image(), b.read_image()) and int(a.read_image().sum()) > 0
-    assert a.read_epochs(ga[1]).sum() > 0        # the backward group was reset inside the replays
+    if S >= 10:   # (6 steps are too few for a backward particle to blow up)
+        assert a.read_epochs(ga[1]).sum() > 0    # the backward group was reset inside the replays
 
 
 def test_capture_restrictions():
@@ -63,6 +64,7 @@ def test_capture_restrictions():
         a.capture(lambda: a.step(10, 0.01))
     assert e.value.status == FF_ERR_STATE
     a.set_reset(True)
-    with pytest.raises(FFError) as e:             # a kernel variant never launched: not compiled yet
+    a.set_launch(1, 512)                          # a kernel variant never launched: not compiled yet
+    with pytest.raises(FFError) as e:
         a.capture(lambda: a.step(1, 0.01))
     assert e.value.status == FF_ERR_STATE
