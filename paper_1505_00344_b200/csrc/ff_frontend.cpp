@@ -1117,7 +1117,7 @@ std::vector<float> eval_program(const UProgram& prog, const std::vector<float>& 
 }
 
 std::string emit_source(const System& s, int sweep_param, int kernel_select, UProgram* prog, bool balance,
-                        bool long_launch) {
+                        bool long_launch, bool thread_redraw) {
   if (sweep_param < -1 || sweep_param >= (int)s.param_names.size())
     throw Error(FF_ERR_INVALID_ARG, "sweep parameter index out of range");
   // pass 1: lower once to find exponentials sharing an affine argument c w + d
@@ -1404,6 +1404,9 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   pre << "#define FF_MINB_P4 " << minb_p4 << "\n";
   pre << "#define FF_SWEEP " << sweep_param << "\n";
   pre << "#define FF_KSEL " << kernel_select << "\n";
+  // reset redraw of the 4-particles-per-thread kernel: per thread for launches of >= 50 steps (nearly
+  // every reset-prone particle resets each launch), warp-cooperative otherwise (ff_reset)
+  pre << "#define FF_THREAD_REDRAW " << (thread_redraw ? 1 : 0) << "\n";
   int packed_bin = 1;
   if (const char* e = std::getenv("FF_TUNE_PACKED_BIN")) packed_bin = std::atoi(e);
   pre << "#define FF_PACKED_BIN " << packed_bin << "\n";

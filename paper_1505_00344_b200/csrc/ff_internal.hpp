@@ -86,7 +86,7 @@ std::vector<float> eval_program(const UProgram& prog, const std::vector<float>& 
 // long_launch: register budget of the packed 128-thread kernel for launches of many steps (systems
 // of <= 4 variables: 40 registers instead of full occupancy's 32).
 std::string emit_source(const System& s, int sweep_param, int kernel_select = 255, UProgram* prog = nullptr,
-                        bool balance = true, bool long_launch = false);
+                        bool balance = true, bool long_launch = false, bool thread_redraw = false);
 
 // NVRTC: source -> sm_100a CUBIN (throws Error(FF_ERR_COMPILE) with the log).
 std::vector<char> compile_cubin(const std::string& source, const std::string& name);

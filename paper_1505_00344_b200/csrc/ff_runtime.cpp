@@ -50,9 +50,10 @@ struct Module {
   cudaKernel_t exchange = nullptr;  // (in base_lib)
   // [variant][id]: variant = balanced + 2 long; balanced = exponentials shared with the FMA pipe,
   // long = the register budget for launches of many steps (emit_source balance, long_launch)
-  cudaLibrary_t step_lib[4][12] = {};
-  cudaKernel_t step[4][12] = {};
-  int occ[4][12] = {};
+  // (+4: the per-thread reset redraw of the 4-particle kernel for launches of >= 50 steps)
+  cudaLibrary_t step_lib[8][12] = {};
+  cudaKernel_t step[8][12] = {};
+  int occ[8][12] = {};
 };
 
 constexpr int kNumStep = 6;
@@ -171,9 +172,9 @@ struct ff_ctx {
     ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize");  // host buffers go out of scope
   }
 
-  cudaLibrary_t load(int sweep, int ksel, bool bal = true, bool long_launch = false) {
-    std::vector<char> cubin =
-        ff::compile_cubin(ff::emit_source(sys, sweep, ksel, nullptr, bal, long_launch), "fireflies_system.cu");
+  cudaLibrary_t load(int sweep, int ksel, bool bal = true, bool long_launch = false, bool thread_redraw = false) {
+    std::vector<char> cubin = ff::compile_cubin(ff::emit_source(sys, sweep, ksel, nullptr, bal, long_launch, thread_redraw),
+                                                "fireflies_system.cu");
     cudaLibrary_t lib = nullptr;
     ck(cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
     return lib;
@@ -195,7 +196,7 @@ struct ff_ctx {
   // step kernel `id` (0-11) of variant v (balanced + 2 long), compiled at its first launch
   cudaKernel_t step_kernel(Module& m, int sweep, int id, int v) {
     if (!m.step[v][id]) {
-      m.step_lib[v][id] = load(sweep, id, (v & 1) != 0, (v & 2) != 0);
+      m.step_lib[v][id] = load(sweep, id, (v & 1) != 0, (v & 2) != 0, (v & 4) != 0);
       const std::string name = std::string(kStepNames[id % kNumStep]) + (id >= kNumStep ? "_c" : "");
       ck(cudaLibraryGetKernel(&m.step[v][id], m.step_lib[v][id], name.c_str()), "cudaLibraryGetKernel(ff_step)");
       int occ = 0;
@@ -210,9 +211,13 @@ struct ff_ctx {
   }
   // the long-launch register budget differs only for the packed 128-thread kernel of systems of
   // <= 4 variables (emit_source long_launch); other kernels share the short variant's module
+  // and the 4-particle kernel's reset redraw is per thread for launches of >= 50 steps (a 100-step
+  // Lorenz frame resets nearly every backward particle: 1029 vs 1051 us), warp-cooperative below
+  // (S = 10: 164 vs 175 us; tools/r02/run23.sh)
   int variant_for(bool bal, int id, int64_t n_steps) const {
     const bool lng = n_steps >= 8 && sys.dim <= 4 && (id % kNumStep == 3 || id % kNumStep == 5);
-    return (bal ? 1 : 0) + (lng ? 2 : 0);
+    const bool thread_redraw = n_steps >= 50 && id % kNumStep == 5;
+    return (bal ? 1 : 0) + (lng ? 2 : 0) + (thread_redraw ? 4 : 0);
   }
   // pipe-balanced (throughput) kernels for launches that fill the GPU; a launch with fewer tiles than
   // two per SM is latency-bound (one particle's RK4 chain is the critical path) and uses MUFU only
@@ -1070,8 +1075,7 @@ ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* pee
     int pp, tt;
     ctx->default_launch(pp, tt, n);
     const int id = step_index(pp, tt);
-    for (int v = 0; v < 4; ++v)
-      if (ctx->variant_for(v & 1, id, (v & 2) ? 100 : 1) == v) ctx->step_kernel(m, ctx->sweep_param, id, v);
+    for (int bal = 0; bal < 2; ++bal) ctx->step_kernel(m, ctx->sweep_param, id, ctx->variant_for(bal != 0, id, n));
   }
   // and force the (lazily loaded) exchange kernel in now: a lazy load at its first launch can wait
   // for the device while a peer's exchange kernel spins waiting for this rank (deadlock on one GPU)

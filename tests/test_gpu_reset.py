@@ -243,14 +243,15 @@ def test_lifted_redraw_uses_a_second_philox_block_at_dim_4():
     assert "%08x" % ctx.read_lifted(g)[case["index"]:].view(np.uint32)[0] == case["lifted_bits"]
 
 
-@pytest.mark.parametrize("ppt,tpb", [(1, 128), (2, 128), (2, 256), (4, 128)])
+@pytest.mark.parametrize("ppt,tpb,steps", [(1, 128, 1), (2, 128, 1), (2, 256, 1), (4, 128, 1), (4, 128, 60)])
 @pytest.mark.parametrize("density", [0.01, 0.2, 0.95])
-def test_redraws_bit_exact_at_any_reset_density(ppt, tpb, density):
+def test_redraws_bit_exact_at_any_reset_density(ppt, tpb, steps, density):
     """The redraw is warp-cooperative when a warp has few resets (jobs spread over the lanes, results
-    shuffled back) and per thread when it has many: both must give the oracle's bits. Particles of a
+    shuffled back; 4-per-thread launches of >= 50 steps redraw per thread instead): both must give the
+    oracle's bits. Particles of a
     4-variable system with a Philox-swept lifted parameter (its redraw needs a second Philox block)
     are poisoned with NaN at random at the given density and stepped with dt = 0 (nothing else
-    moves): every poisoned particle is redrawn exactly as the oracle's reset rule with its epoch
+    moves; 60 steps select the long-launch build): every poisoned particle is redrawn exactly as the oracle's reset rule with its epoch
     (state and lifted value), every other one keeps its bits."""
     from paper_1505_00344_b200.systems import SystemDef
     sysdef = SystemDef("lin4", ["a", "b", "c", "d"], ["k*a", "k*b", "k*c", "k*d"], [("k", 0.0, None, None)])
@@ -269,7 +270,7 @@ def test_redraws_bit_exact_at_any_reset_density(ppt, tpb, density):
         st = before.copy()
         st[:, sel] = np.nan
         ctx.write_state(g, st)
-        ctx.step(1, 0.0)
+        ctx.step(steps, 0.0)
         ep, got, lifted = ctx.read_epochs(g), ctx.read_state(g), ctx.read_lifted(g)
         assert np.array_equal(ep, prev_ep + sel.astype(np.uint32))
         keep = ~sel
