@@ -165,7 +165,7 @@ def setup(args, w, rank, world):
     if w.get("prerun"):
         ctx.step(w["prerun"], w["dt"])
     axes, view = projection(w)
-    fused = not args.no_image and (args.exchange in ("fused", "nvls") or (args.exchange == "auto" and world > 1))
+    fused = not args.no_image and (args.exchange == "fused" or (args.exchange in ("auto", "nvls") and world > 1))
     img = None
     if fused:   # the image sum over ranks is done by the library after each launch, no NCCL call
         from paper_1505_00344_b200 import dist as ffdist
