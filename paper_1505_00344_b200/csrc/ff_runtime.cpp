@@ -45,8 +45,7 @@ struct Module {
   cudaKernel_t render = nullptr;
   cudaKernel_t lifted = nullptr;     // ff_read_lifted
   // step kernels by (ppt, tpb): 0 p1t128, 1 p1t256, 2 p1t512, 3 p2t128, 4 p2t256, 5 p4t128;
-  // +6 = the same with position-linear colour compiled in (ff_project_colour), +12 = with the fused
-  // image exchange (ff_set_exchange)
+  // +6 = the same with position-linear colour compiled in (ff_project_colour)
   cudaKernel_t exchange = nullptr;  // (in base_lib)
   // [variant][id]: variant = balanced + 2 long; balanced = exponentials shared with the FMA pipe,
   // long = the register budget for launches of many steps (emit_source balance, long_launch)
