@@ -458,6 +458,30 @@ def single_core_oracle(config, n, S):
         return {"error": str(e)[:200]}
 
 
+def o3_native_oracle(config, n, S):
+    """The same oracle source built -O3 -march=native on this host (oracle/build.py build_timing;
+    SURVEY.md 8(d) "oracle timing"), all cores, in a child process: how much of the GPU/CPU ratio is
+    compiler flags. Context only."""
+    import subprocess
+    import tempfile
+    from oracle import build as obuild
+    code = ("import sys; sys.argv=['bench']; import bench; "
+            f"bench.cpu_oracle_sample(bench.WORKLOADS[{config!r}], {max(256, int(n) // 16)}, {int(S)}); "   # warm-up
+            f"v, dt, t, n = bench.cpu_oracle_sample(bench.WORKLOADS[{config!r}], {int(n)}, {int(S)}); "
+            "print(v, dt, t, n)")
+    try:
+        with tempfile.TemporaryDirectory() as d:
+            lib = obuild.build_timing(d)
+            out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300,
+                                 env=dict(os.environ, FF_ORACLE_LIB=lib))
+            v, dt, t, n = out.stdout.split()
+        return {"value": float(v), "unit": "particle-steps/s", "cores": int(t),
+                "sample": f"{int(n)} particles x {S} RK4 steps + binning ({float(dt):.1f} s)",
+                "build": "same source, gcc -O3 -march=native -ffp-contract=off, OpenMP"}
+    except Exception as e:   # context only; never fail the bench line over it
+        return {"error": str(e)[:200]}
+
+
 def reference_sample_size(w, S):
     # bounded sample: ~5-12 s of the oracle on a 16-core host (Lorenz ~5e8, STN-GPe ~1.4e8, HH ring
     # ~3.6e7 particle-steps/s measured), i.e. several frames' worth of the workload's particles
@@ -663,7 +687,8 @@ def main():
                                 "build": "the scalar oracle as it stands (plain C, gcc -O2 -ffp-contract=off, "
                                          "OpenMP over particles, no SIMD): a correctness reference, not a tuned "
                                          "CPU implementation -- the GPU/CPU ratio is context only",
-                                "single_core": single_core_oracle(args.config, max(1024, n // 32), r["S"])}
+                                "single_core": single_core_oracle(args.config, max(1024, n // 32), r["S"]),
+                                "o3_native": o3_native_oracle(args.config, n, r["S"])}
     print(json.dumps(line))
 
 

@@ -36,7 +36,8 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        path = _build.build()
+        # FF_ORACLE_LIB: a timing build of the same source (oracle/build.py build_timing; bench.py only)
+        path = os.environ.get("FF_ORACLE_LIB") or _build.build()
         L = C.CDLL(path)
         P = C.c_void_p
         i64 = C.c_int64
