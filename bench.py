@@ -29,7 +29,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "particle-steps/s per B200 and per box (Lorenz RK4, 15-D neuron); % FP32 peak"
 N_SM = 148
-FMA_LANES = 128   # FP32 lanes per SM (FFMA2 does not raise it: profiles/r01_ubench_pipes.txt)
+FMA_LANES = 128   # FP32 lanes per SM (FFMA2 does not raise it: profiles/r02_ubench_pipes.txt)
 XU_LANES = 16     # MUFU results per clock per SM (same microbenchmark)
 RED_PEAK = 2.21e11    # L2 reductions / s on 4 M distinct words (tools/ubench/pipes.cu, profiles/r02_ubench_pipes.txt)
 # stream + reductions in one kernel (tools/ubench/red_stream.cu, profiles/r02_ubench_red_stream.txt)
@@ -624,7 +624,7 @@ def main():
         "alu": (per_launch * work / kern_s, N_SM * FMA_LANES * f_max,
                 "Tops/s (FP32-pipe-equivalent lane-ops of the pipe-balanced work, a*b+c = 1 op)",
                 f"148 SM x 128 FP32 lanes x {f_max / 1e6:.0f} MHz (MEASURED_PEAKS sm_max_mhz; FFMA2 / FADD2 / "
-                "FMUL2 measured at 126 lane-ops/clk/SM, MUFU 16/clk/SM: profiles/r01_ubench_pipes.txt)", work),
+                "FMUL2 measured at 126 lane-ops/clk/SM, MUFU 16/clk/SM: profiles/r02_ubench_pipes.txt)", work),
         "hbm": (r["n_local"] * 8 * dim / kern_s, peaks.get("hbm_gbs", 6549.1) * 1e9, "GB/s",
                 "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)", 8 * dim / r["S"]),
     }
