@@ -211,6 +211,14 @@ PACKED_KERNEL(k_fadd2_2reg, c[i] = make_float2(-c[i].x * 1e-9f, c[i].y * 1e-9f),
 PACKED_KERNEL(k_ffma2_rscalar, b[i] = make_float2(1.0f + threadIdx.x * 1e-9f + i * 1e-8f, 0.f),
               a[i] = __ffma2_rn(make_float2(b[i].x, b[i].x), a[i], c[i]))
 PACKED_KERNEL(k_fmul2_2reg, b[i] = make_float2(1.0000001f, 0.9999999f), a[i] = __fmul2_rn(a[i], b[i]))
+// operand kinds of the HH ring loop: one pair + a per-thread register scalar + an
+// immediate (c1 v + c2 with c1 in a register), one pair + two register scalars (q-table constants
+// that ptxas kept in registers), two pairs + a register scalar per accumulator
+PACKED_KERNEL(k_ffma2_p1r1k, b[i] = make_float2(0.999f + threadIdx.x * 1e-9f + i * 1e-8f, 0.f),
+              a[i] = __ffma2_rn(a[i], make_float2(b[i].x, b[i].x), make_float2(0.25f, 0.25f)))
+PACKED_KERNEL(k_ffma2_p1r2, (b[i] = make_float2(0.999f + threadIdx.x * 1e-9f + i * 1e-8f, 0.f),
+                             c[i] = make_float2(0.25f + threadIdx.x * 1e-9f, 0.f)),
+              a[i] = __ffma2_rn(a[i], make_float2(b[i].x, b[i].x), make_float2(c[i].x, c[i].x)))
 
 typedef void (*kfn)(const float*, float*, long long*);
 
@@ -263,6 +271,8 @@ int main() {
     run("FADD2(2reg)", k_fadd2_2reg, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
     run("FMUL2(2reg)", k_fmul2_2reg, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
     run("FFMA2(Rscal)", k_ffma2_rscalar, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
+    run("FFMA2(p1r1k)", k_ffma2_p1r1k, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
+    run("FFMA2(p1r2)", k_ffma2_p1r2, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
     run("MUFU.EX2", k_ex2, NACC, ITERS / 4, nsm, 1024, din, dout, dcyc);
     run("MUFU.RCP", k_rcp, NACC, ITERS / 4, nsm, 1024, din, dout, dcyc);
     run("FFMA4+EX2", k_mix, 5 * NACC, ITERS / 4, nsm, 1024, din, dout, dcyc);
