@@ -653,3 +653,44 @@ def test_poisoned_neighbours_do_not_leak(name, make, lo, hi, sweep, axes):
     assert np.array_equal(dirty[:, ~bad].view(np.uint32), clean[:, ~bad].view(np.uint32))
     want = O.histogram(dirty, axes, view, 256, 256, 1, 0)
     assert np.array_equal(img, want)
+
+
+@pytest.mark.parametrize("seed", list(range(12)))
+@pytest.mark.parametrize("ppt,tpb", [(2, 128), (4, 128), (1, 128)])
+def test_histogram_3d_random_cameras_and_magnitudes_bit_exact(seed, ppt, tpb):
+    """Fuzz of the 3-D binning (reading R18) through the packed pair path (2 and 4 particles per thread:
+    FMUL2 / FFMA2 sums, shared reciprocal, ff_div2_pair) and the scalar one: random view-projection
+    matrices -- perspective, orthographic-like, and dense random ones with entries over 12 orders of
+    magnitude -- and coordinates mixing ordinary values, huge and tiny magnitudes, exact zeros,
+    values on pixel edges, infinities and NaN, so both the fast division box and its div.rn fallback
+    are hit; the image must equal the oracle's histogram of the same coordinates bit for bit."""
+    rng = np.random.default_rng(1000 + seed)
+    n = 24000 + seed
+    ctx = lorenz_ctx([n])
+    ctx.set_launch(ppt, tpb)
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=1)
+    W, H = int(rng.integers(17, 700)), int(rng.integers(13, 500))
+    kind = seed % 3
+    if kind == 0:
+        eye = rng.uniform(-150, 150, 3)
+        Mv = views.look_at(tuple(eye), tuple(rng.uniform(-10, 10, 3)), (0.0, 0.0, 1.0))
+        M = (views.perspective(float(rng.uniform(10, 120)), W / H, 0.1, 5000.0) @ Mv).astype(np.float32)
+    elif kind == 1:
+        M = np.diag(rng.uniform(0.01, 0.2, 4)).astype(np.float32)
+        M[3] = [0.0, 0.0, 0.0, 1.0]
+        M[:3, 3] = rng.uniform(-1, 1, 3)
+    else:
+        M = (rng.standard_normal((4, 4)) * 10.0 ** rng.uniform(-6, 6, (4, 4))).astype(np.float32)
+    x = np.stack([rng.uniform(-40, 40, n), rng.uniform(-60, 60, n), rng.uniform(-10, 80, n)]).astype(np.float32)
+    pick = rng.random((3, n))
+    x[pick < 0.05] *= np.float32(1e25)
+    x[(pick >= 0.05) & (pick < 0.10)] *= np.float32(1e-25)
+    x[(pick >= 0.10) & (pick < 0.12)] = 0.0
+    x[(pick >= 0.12) & (pick < 0.13)] = np.inf
+    x[(pick >= 0.13) & (pick < 0.14)] = -np.inf
+    x[(pick >= 0.14) & (pick < 0.15)] = np.nan
+    ctx.write_state(g, x)
+    ctx.project([0, 1, 2], M, W, H, 1)
+    want = O.histogram(x, [0, 1, 2], M, W, H, 1, 0)
+    got = ctx.read_image()
+    assert np.array_equal(got, want), f"{np.count_nonzero(got != want)} pixels differ (kind {kind})"
