@@ -45,8 +45,15 @@ def oracle_image(ctx, gids, w, sysdef):
     return want
 
 
+# variants of the bench workloads that exercise the other sweep mode with the reset rule
+EXTRA = {"sweep_linspace_reset": dict(bench.WORKLOADS["sweep"], sweep=("r", 0.0, 200.0, 1, 5),
+                                      reset=(None, None, 0.0)),
+         "sweep_philox_reset_bounds": dict(bench.WORKLOADS["sweep"], reset=([-60.0, -80.0, -20.0],
+                                                                            [60.0, 80.0, 120.0], 0.0))}
+
+
 def frame(name, S):
-    w = bench.WORKLOADS[name]
+    w = EXTRA.get(name) or bench.WORKLOADS[name]
     ctx, gids, img, _ = bench.setup(ARGS, w, 0, 1)
     img.zero_()
     ctx.step(S, w["dt"])
@@ -55,7 +62,8 @@ def frame(name, S):
 
 
 @pytest.mark.parametrize("name,S", [("lorenz3d", 100), ("lorenz3d", 10), ("lorenz3d", 1), ("sweep", 100),
-                                    ("hh", 100), ("stn_bif3d", 100)])
+                                    ("hh", 100), ("stn_bif3d", 100), ("stn", 1000), ("lorenz3d_collapsed", 100),
+                                    ("sweep_linspace_reset", 100), ("sweep_philox_reset_bounds", 100)])
 def test_bench_frame_image_is_oracle_histogram_of_its_state(name, S):
     w, ctx, gids, img = frame(name, S)
     sysdef = bench.make_system(w["system"])
