@@ -243,19 +243,24 @@ def test_lifted_redraw_uses_a_second_philox_block_at_dim_4():
     assert "%08x" % ctx.read_lifted(g)[case["index"]:].view(np.uint32)[0] == case["lifted_bits"]
 
 
-@pytest.mark.parametrize("ppt,tpb,steps", [(1, 128, 1), (2, 128, 1), (2, 256, 1), (4, 128, 1), (4, 128, 60)])
+@pytest.mark.parametrize("dim,ppt,tpb,steps", [(4, 1, 128, 1), (4, 2, 128, 1), (4, 2, 256, 1), (4, 4, 128, 1),
+                                               (4, 4, 128, 60), (9, 1, 128, 1), (9, 2, 128, 1), (9, 2, 128, 60)])
 @pytest.mark.parametrize("density", [0.01, 0.2, 0.95])
-def test_redraws_bit_exact_at_any_reset_density(ppt, tpb, steps, density):
+def test_redraws_bit_exact_at_any_reset_density(dim, ppt, tpb, steps, density):
     """The redraw is warp-cooperative when a warp has few resets (jobs spread over the lanes, results
     shuffled back; 4-per-thread launches of >= 50 steps redraw per thread instead): both must give the
-    oracle's bits. Particles of a
-    4-variable system with a Philox-swept lifted parameter (its redraw needs a second Philox block)
-    are poisoned with NaN at random at the given density and stepped with dt = 0 (nothing else
-    moves; 60 steps select the long-launch build): every poisoned particle is redrawn exactly as the oracle's reset rule with its epoch
+    oracle's bits. Particles of a 4- or 9-variable system with a Philox-swept lifted parameter (its
+    redraw needs a second / third Philox block; 9 variables shuffle 10 values per job) are poisoned
+    with NaN at random at the given density and stepped with dt = 0 (nothing else moves; 60 steps
+    select the long-launch build): every poisoned particle is redrawn exactly as the oracle's reset
+    rule with its epoch
     (state and lifted value), every other one keeps its bits."""
     from paper_1505_00344_b200.systems import SystemDef
-    sysdef = SystemDef("lin4", ["a", "b", "c", "d"], ["k*a", "k*b", "k*c", "k*d"], [("k", 0.0, None, None)])
-    lo, hi, seed, sseed = [-1.0, 0.0, 2.0, -5.0], [1.0, 3.0, 2.5, 5.0], 31, 77
+    names = ["v%d" % d for d in range(dim)]
+    sysdef = SystemDef("lin%d" % dim, names, ["k*" + v for v in names], [("k", 0.0, None, None)])
+    lo = ([-1.0, 0.0, 2.0, -5.0] * 3)[:dim]
+    hi = ([1.0, 3.0, 2.5, 5.0] * 3)[:dim]
+    seed, sseed = 31, 77
     n = 20000 + 37
     ctx = FF.Context(sysdef, [n])
     ctx.set_launch(ppt, tpb)
@@ -277,7 +282,7 @@ def test_redraws_bit_exact_at_any_reset_density(ppt, tpb, steps, density):
         assert np.array_equal(got[:, keep].view(np.uint32), before[:, keep].view(np.uint32))
         assert np.array_equal(lifted[keep].view(np.uint32), lifted0[keep].view(np.uint32))
         for i in np.nonzero(sel)[0]:
-            col = np.full((4, 1), np.nan, np.float32)
+            col = np.full((dim, 1), np.nan, np.float32)
             sv = np.zeros(1, np.float32)
             O.reset(col, None, None, 0.0, 0.0, np.zeros(1, np.float32), np.array([ep[i] - 1], np.uint32), lo, hi,
                     seed, first_global=int(i), sweep=dict(vals=sv, lo=0.5, hi=1.5, mode=0, seed=sseed, n_group=n))
