@@ -1384,10 +1384,11 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   int minb_p2_t128 = dim <= 4 ? 12 : (dim <= 8 ? 4 : 2);
   (void)long_launch;
   if (const char* e = std::getenv("FF_TUNE_MINB_P2_T128")) minb_p2_t128 = std::atoi(e);
-  // 4 particles per thread, 128-thread blocks: 1-4-step launches without an image (memory-bound,
-  // Lorenz 76 registers at 6 blocks/SM); long launches of FMA-bound small systems at 8 blocks /
-  // <= 64 registers (two FFMA2 chains per thread: Lorenz S = 100 8.22 -> 8.41e11, tools/r01/gpu_run76.sh)
-  int minb_p4 = dim <= 4 ? (long_launch ? 8 : 6) : (dim <= 8 ? 2 : 1);
+  // 4 particles per thread, 128-thread blocks, 8 blocks / <= 64 registers: 1-4-step launches of small
+  // systems, with or without an image (memory / L2-bound; round 1 ran them at 6 blocks: S = 1 without
+  // an image 44 -> 39 us, with one 79 -> 75 us, tools/r02/run45.sh), and long launches of FMA-bound
+  // small systems (two FFMA2 chains per thread: Lorenz S = 100 8.22 -> 8.41e11, tools/r01/gpu_run76.sh)
+  int minb_p4 = dim <= 4 ? 8 : (dim <= 8 ? 2 : 1);
   if (const char* e = std::getenv("FF_TUNE_MINB_P4")) minb_p4 = std::atoi(e);
   // tuning knobs for experiments (not part of the ABI): FF_TUNE_MINB_P2, FF_TUNE_UNROLL
   if (const char* e = std::getenv("FF_TUNE_MINB_P2")) minb_p2 = std::atoi(e);

@@ -261,19 +261,21 @@ struct ff_ctx {
   }
 
   void default_launch(int& ppt_out, int& tpb_out, int64_t n_steps = 100) {
-    // memory-bound launches (1-4 steps, no image) of small systems: 16-byte vector I/O, 4 particles
-    // per thread; with an image bound the histogram atomics dominate and the full-occupancy packed
-    // kernel below hides them better (measured: 9.0e10 vs 7.8e10 particle-steps/s at S = 1)
-    if (!ppt && !tpb && sys.dim <= 4 && n_steps <= 4 && !image) {
-      ppt_out = 4;
-      tpb_out = 128;
-      return;
-    }
     // too few particles to give every SM a 256-particle tile: the launch is latency-bound (each
     // particle's RK4 chain is the critical path), so spread it over as many SMs as possible with one
     // particle per thread (configs[0], 10 k STN-GPe particles: 1.9x faster than packed pairs)
     if (!ppt && !tpb && next_slot < 256 * (int64_t)nsm) {
       ppt_out = 1;
+      tpb_out = 128;
+      return;
+    }
+    // short launches (1-4 steps) of small systems, with or without an image: 16-byte vector I/O, 4
+    // particles per thread, 8 blocks/SM (round 2, tools/r02/run45.sh, Lorenz 8.4 M with the reset
+    // rule: S = 1 with image 91 -> 75 us against packed pairs, S = 2 / 4 109 -> 99 / 121 -> 113 us,
+    // no image S = 1 44 -> 39 us; STN-GPe bifurcation S = 1 146 -> 138 us. Round 1 kept pairs when an
+    // image was bound: its projection and histogram code was heavier.)
+    if (!ppt && !tpb && sys.dim <= 4 && n_steps <= 4) {
+      ppt_out = 4;
       tpb_out = 128;
       return;
     }
