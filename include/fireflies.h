@@ -239,7 +239,7 @@ ff_status ff_read_lifted(ff_ctx* ctx, int group_id, int64_t first, int64_t count
  * 16-byte loads) and threads per block (128, 256 or 512; 4 particles only with 128); 0 = library
  * default: one particle per thread in 128-thread blocks when the groups hold fewer than 256
  * particles per SM (latency-bound); for systems with <= 4 variables 4 per thread for 1-4-step
- * launches (HBM / L2-bound) and for launches of >= 8 steps of systems without MUFU work; else packed
+ * launches (HBM / L2-bound) and for longer launches of systems without MUFU work; else packed
  * pairs. Results are the same for every choice up to FP rounding (the projection,
  * counting and reset draws bit for bit). For tuning/benchmarks. Errors: FF_ERR_INVALID_ARG. */
 ff_status ff_set_launch(ff_ctx* ctx, int particles_per_thread, int threads_per_block);

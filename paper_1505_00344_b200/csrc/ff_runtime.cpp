@@ -284,10 +284,11 @@ struct ff_ctx {
     // >= 4 tiles of 512 per SM run 256-thread blocks (fewer tile fetches and block barriers per
     // particle: Lorenz S = 100 8.13 -> 8.22e11), shorter ones 128-thread blocks (S = 10: 5.42 vs 5.34e11)
     const bool wide = n_steps >= 50 && next_slot >= 4 * 512 * (int64_t)nsm;
-    // FMA-bound small systems (no MUFU op): long launches run 4 particles per thread (two independent
-    // FFMA2 chains, 8 blocks / <= 64 registers): Lorenz S = 10 / 100 / 1000 +4 / +2.3 / +2.8%; a
-    // MUFU-bound one (STN-GPe) loses 6% there (tools/r01/gpu_run76.sh)
-    if (!ppt && !tpb && sys.dim <= 4 && n_steps >= 8 && next_slot >= 4 * 512 * (int64_t)nsm &&
+    // FMA-bound small systems (no MUFU op): longer launches run 4 particles per thread too (two
+    // independent FFMA2 chains, 8 blocks / <= 64 registers): Lorenz S = 7 / 10 / 100 / 1000: -7% / -4% /
+    // -2.3% / -2.8% time (tools/r01/gpu_run76.sh, tools/r02/run49.sh); a MUFU-bound one (STN-GPe) loses
+    // 4-6% there from 10 steps on
+    if (!ppt && !tpb && sys.dim <= 4 && next_slot >= 4 * 512 * (int64_t)nsm &&
         uprogram(sweep_param, true).mufu_per_step == 0) {
       ppt_out = 4;
       tpb_out = 128;
