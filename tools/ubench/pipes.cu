@@ -98,6 +98,31 @@ __global__ void k_fadd(const float* __restrict__ in, float* out, long long* cyc)
 __device__ __forceinline__ float ex2(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ float rcp(float x) { float y; asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 
+// 32 x 32 -> 64-bit multiply (IMAD.WIDE.U32) + 3-input XOR: one Philox4x32 half-round, the reset
+// redraw's inner loop (what a reset costs)
+__global__ void k_imadwide(const float* __restrict__ in, float* out, long long* cyc) {
+  unsigned a[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) a[i] = __float_as_uint(in[2 + i]) + threadIdx.x * 7919u + i;
+  __syncthreads();
+  long long t0 = clock64();
+#pragma unroll 2
+  for (int it = 0; it < ITERS / 4; ++it) {
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) {
+      const unsigned long long p = (unsigned long long)a[i] * 0xD2511F53ull;
+      a[i] = (unsigned)(p >> 32) ^ (unsigned)p ^ 0x9E3779B9u;
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  unsigned s = 0;
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (float)s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 __global__ void k_ex2(const float* __restrict__ in, float* out, long long* cyc) {
   float a[NACC];
 #pragma unroll
@@ -274,6 +299,7 @@ int main() {
     run("FFMA2(p1r1k)", k_ffma2_p1r1k, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
     run("FFMA2(p1r2)", k_ffma2_p1r2, 2 * NACC, ITERS, nsm, 1024, din, dout, dcyc);
     run("MUFU.EX2", k_ex2, NACC, ITERS / 4, nsm, 1024, din, dout, dcyc);
+    run("IMAD.WIDE", k_imadwide, NACC, ITERS / 4, nsm, 1024, din, dout, dcyc);
     run("MUFU.RCP", k_rcp, NACC, ITERS / 4, nsm, 1024, din, dout, dcyc);
     run("FFMA4+EX2", k_mix, 5 * NACC, ITERS / 4, nsm, 1024, din, dout, dcyc);
   }
