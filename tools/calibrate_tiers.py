@@ -58,6 +58,36 @@ def main():
                    "p99.99": float(np.percentile(e, 99.99)), "tier_a_holds": bool(e.max() <= 1e-5)}
             out["cases"].append(row)
             print(row)
+    # HH ring N = 3 (readings R7-R11), configs[2]: 2^20 particles in the bench; proxy on n particles
+    hh_names = O.hh_param_names(3)
+    hh_vals = dict(C=1.0, g_na=120.0, g_k=36.0, g_lk=0.3, e_na=115.0, e_k=-12.0, e_lk=10.613, g_syn=0.5,
+                   e_syn=10.0, tau_r=0.5, tau_d=3.0, sigma=5.0, theta=20.0, I1=10.0, I2=10.0, I3=10.0)
+    ph = np.array([hh_vals[k] for k in hh_names])
+    hlo, hhi = [-20.0, 0, 0, 0, 0] * 3, [100.0, 1, 1, 1, 1] * 3
+    hscale = np.maximum(np.maximum(np.abs(np.array(hlo)), np.abs(np.array(hhi))), 1.0)
+    z0 = O.ic_uniform(hlo, hhi, 4, 0, min(n, 20000))
+    for steps in (10, 30, 100):
+        a = O.rk4(O.HH, z0, ph.astype(np.float32), np.float32(0.01), steps)
+        b = O.rk4(O.HH, z0.astype(np.float64), ph, float(np.float32(0.01)), steps)
+        e = scaled_err(a, b, hscale).max(axis=0)
+        row = {"case": "hh_ring3", "steps": steps, "finite_fraction": float(np.isfinite(b).all(axis=0).mean()),
+               "max": float(e.max()), "p99": float(np.percentile(e, 99)),
+               "p99.99": float(np.percentile(e, 99.99)), "tier_a_holds": bool(e.max() <= 1e-5)}
+        out["cases"].append(row)
+        print(row)
+    # Lorenz with r swept over [0, 200) (Philox, configs[3]), sigma and beta as config 2
+    sv = O.sweep_values(0.0, 200.0, 0, 5, 0, n, n)
+    x0s = O.ic_uniform(LO, HI, 5, 0, n)
+    ps = np.array([10.0, 0.0, 8.0 / 3.0])
+    for steps in (10, 30):
+        a = O.rk4(O.LORENZ, x0s, ps.astype(np.float32), np.float32(0.01), steps, 1, sv)
+        b = O.rk4(O.LORENZ, x0s.astype(np.float64), ps, float(np.float32(0.01)), steps, 1, sv.astype(np.float64))
+        e = scaled_err(a, b, scale).max(axis=0)
+        row = {"case": "lorenz_swept_r", "steps": steps, "finite_fraction": 1.0, "max": float(e.max()),
+               "p99": float(np.percentile(e, 99)), "p99.99": float(np.percentile(e, 99.99)),
+               "tier_a_holds": bool(e.max() <= 1e-5)}
+        out["cases"].append(row)
+        print(row)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     json.dump(out, open(os.path.join(ROOT, "profiles", "r02_tier_calibration.json"), "w"), indent=1)
 
