@@ -1408,9 +1408,6 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   // reset redraw of the 4-particles-per-thread kernel: per thread for launches of >= 50 steps (nearly
   // every reset-prone particle resets each launch), warp-cooperative otherwise (ff_reset)
   pre << "#define FF_THREAD_REDRAW " << (thread_redraw ? 1 : 0) << "\n";
-  int packed_bin = 1;
-  if (const char* e = std::getenv("FF_TUNE_PACKED_BIN")) packed_bin = std::atoi(e);
-  pre << "#define FF_PACKED_BIN " << packed_bin << "\n";
 
   std::string tmpl(kDeviceTemplate);
   const std::string marker = "#include_generated_rhs";
