@@ -10,9 +10,12 @@ perspective density image 1024 x 1024 x 2 channels, S = 100 steps per frame.
                   [--S steps_per_frame] [--impl ours|reference]
 
 Under torchrun (N > 1) every rank runs the same per-rank workload on its shard (weak scaling) and
-the per-frame image is summed over the ranks (the path's one exchange step) by the
-library's exchange kernel over peer memory (--exchange auto, validated on one frame, else an NCCL
-all-reduce; --exchange nccl|fused forces one); the time is the max over ranks. --impl reference
+the per-frame image is summed over the ranks (the path's one exchange step): by an
+NCCL all-reduce inside the frame's events (default, --exchange nccl), or by the library itself --
+its exchange kernel over peer memory after each launch (fused; auto = validated on one frame, else
+NCCL; nvls = its sum pass through NVSwitch multicast) or the histogram's own reductions sent to every
+rank's image (push; nvls-push = as multimem.red through the multicast address); the time is the max
+over ranks. --impl reference
 times the CPU oracle (the tier's reference arm) on a bounded sample of the same workload.
 """
 import argparse
@@ -165,22 +168,24 @@ def setup(args, w, rank, world):
     if w.get("prerun"):
         ctx.step(w["prerun"], w["dt"])
     axes, view = projection(w)
-    fused = not args.no_image and (args.exchange == "fused" or (args.exchange in ("auto", "nvls") and world > 1))
+    fused = not args.no_image and (args.exchange in ("fused", "push") or
+                                   (args.exchange in ("auto", "nvls", "nvls-push") and world > 1))
     img = None
     if fused:   # the image sum over ranks is done by the library after each launch, no NCCL call
         from paper_1505_00344_b200 import dist as ffdist
         try:
-            if args.exchange == "nvls":   # NVSwitch multicast sum pass (multimem), torch symmetric memory
-                img = ffdist.bind_exchanged_image(ctx, axes, view, w["W"], w["H"], w["C"], mapping="symmetric",
-                                                  multicast=True)
-            else:
-                img = ffdist.bind_exchanged_image(ctx, axes, view, w["W"], w["H"], w["C"])
-            if args.exchange in ("auto", "nvls"):
+            # nvls: NVSwitch multicast (torch symmetric memory); push: the histogram's reductions go to
+            # every rank's image (ff_set_exchange_push) instead of a sum pass after the launch
+            mc = args.exchange in ("nvls", "nvls-push")
+            img = ffdist.bind_exchanged_image(ctx, axes, view, w["W"], w["H"], w["C"],
+                                              mapping="symmetric" if mc else "auto", multicast=mc,
+                                              push=args.exchange in ("push", "nvls-push"))
+            if args.exchange in ("auto", "nvls", "nvls-push"):
                 ok, why = validate_exchange(ctx, img, w)
                 if not ok:
                     raise RuntimeError(why)
         except Exception as e:   # auto: fall back to the NCCL all-reduce, say why in the line
-            if args.exchange == "fused":
+            if args.exchange in ("fused", "push"):
                 raise
             args.exchange_note = f"library exchange ({args.exchange}) unavailable ({str(e)[:160]}); NCCL all-reduce used"
             ctx.set_exchange(0, 0)
@@ -526,12 +531,15 @@ def main():
                     help="L2 flush between timed frames (default: read 256 MiB; 'none' only for experiments)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-reset", action="store_true", help="(experiments) leave the workload's reset rule off")
-    ap.add_argument("--exchange", default="nccl", choices=["auto", "nccl", "fused", "nvls"],
+    ap.add_argument("--exchange", default="nccl", choices=["auto", "nccl", "fused", "nvls", "push", "nvls-push"],
                     help="per-frame image sum over ranks (N > 1): an NCCL all-reduce (default), or the "
                          "library's exchange over peer memory after each launch (ff_set_exchange; 'auto' "
                          "validates it once and falls back to NCCL) -- not the default until it has run "
                          "across physical GPUs; 'nvls' = the library exchange with its sum pass through "
-                         "NVSwitch multicast (multimem), validated likewise")
+                         "NVSwitch multicast (multimem), validated likewise; 'push' = the fused exchange "
+                         "(ff_set_exchange_push: the histogram's reductions sent to every rank's image over "
+                         "peer memory, no sum pass), 'nvls-push' = the same as multimem.red through the "
+                         "multicast address, validated with NCCL fallback")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = WORKLOADS[args.config]
@@ -590,12 +598,16 @@ def main():
               f"{backend}, NCCL {nccl})", file=sys.stderr, flush=True)
     r = run_ours(args, w, rank, world, device)
     if world > 1:
+        how = {"nvls": "image sum by the library's exchange kernel (NVLS multimem sum pass) after each launch",
+               "push": "image sum by the histogram itself: its reductions go to every rank's image over NVLink "
+                       "peer memory (ff_set_exchange_push), a barrier before and after each launch",
+               "nvls-push": "image sum by the histogram itself: its reductions go once each to the images' NVLS "
+                            "multicast address (multimem.red), a barrier before and after each launch"}
         config["parallelism"] = f"particles sharded over {world} GPU(s), " + (
-            ("image sum by the library's exchange kernel (NVLS multimem sum pass) after each launch"
-             if args.exchange == "nvls" else
-             "image sum by the library's exchange kernel over NVLink peer memory after each launch")
+            how.get(args.exchange, "image sum by the library's exchange kernel over NVLink peer memory after each launch")
             if r["fused"] else "NCCL image all-reduce per frame")
-        config["exchange"] = ("library-nvls" if args.exchange == "nvls" else "library") if r["fused"] else "nccl"
+        config["exchange"] = ({"nvls": "library-nvls", "push": "library-push", "nvls-push": "library-nvls-push"}
+                              .get(args.exchange, "library") if r["fused"] else "nccl")
         if getattr(args, "exchange_note", None):
             config["exchange_note"] = args.exchange_note
     if world > 1:

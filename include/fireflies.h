@@ -334,6 +334,26 @@ ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* pee
  * (misaligned). */
 ff_status ff_set_exchange_multicast(ff_ctx* ctx, uint32_t* mc_image);
 
+/* Fused (push) variant of the image exchange (SURVEY.md 8(e) "Fused option", 8(f) NEXT 2): after
+ * ff_set_exchange, on = 1 makes the histogram of every binning launch send its reductions straight to
+ * every rank's image -- no sum pass. mc_image = NULL: each reduction is issued once per rank as a
+ * system-scope red.add over peer memory to peer_images[p] (on one GPU, other contexts' images);
+ * mc_image = the NVLS multicast address of the images (as for ff_set_exchange_multicast): each is
+ * issued once as multimem.red.add and the NVSwitch applies it to every rank's copy. Each pushing
+ * launch runs between two barriers over the ranks (kernel ff_xbarrier on the exchange's signal
+ * words): before it every rank has finished what it issued earlier on its stream (zeroing or reading
+ * its image), after it every rank's reductions are in every image. Semantics differ from the sum
+ * pass: the launch ADDS the sum over ranks of its counts to every rank's image (previous contents
+ * kept, not summed), so images that start equal (e.g. zeroed on every rank each frame) stay equal and
+ * equal the unsharded run's image after any sequence of launches -- bit-exact, integer. on = 0
+ * returns to the sum pass. Collective like ff_set_exchange (every rank, same on / kind of address,
+ * no exchanged launch in flight); compiles the pushing kernels on the spot. Needs world >= 2 to
+ * change anything (one rank: its image already is the sum). The multicast form needs a
+ * multicast-capable NVSwitch system (refused on a single GPU). ff_set_exchange and rebinding the image
+ * turn it off. Errors: FF_ERR_STATE (no exchange set), FF_ERR_INVALID_ARG (on not 0/1, misaligned),
+ * FF_ERR_COMPILE, FF_ERR_CUDA. */
+ff_status ff_set_exchange_push(ff_ctx* ctx, int on, uint32_t* mc_image);
+
 /* Upper bound on the blocks of every step and exchange launch (0 = the default: every resident block
  * for a step, 2 per SM for an exchange). For several ranks sharing one GPU (their exchanges must run
  * concurrently), and for tuning. Errors: FF_ERR_INVALID_ARG. */

@@ -25,7 +25,7 @@ EXPORTS = ["ff_last_error", "ff_abi_version", "ff_build_info", "ff_emit_source",
            "ff_set_param", "ff_get_param", "ff_sweep_param", "ff_project", "ff_step", "ff_set_reset",
            "ff_read_epochs", "ff_read_lifted", "ff_set_launch",
            "ff_read_state", "ff_write_state", "ff_read_image", "ff_render", "ff_project_colour", "ff_launch_count", "ff_sync",
-           "ff_set_exchange", "ff_set_exchange_multicast", "ff_set_grid_limit", "ff_write_state_async", "ff_read_image_async"]
+           "ff_set_exchange", "ff_set_exchange_multicast", "ff_set_exchange_push", "ff_set_grid_limit", "ff_write_state_async", "ff_read_image_async"]
 
 
 class FFError(RuntimeError):
@@ -87,6 +87,7 @@ def lib():
             "ff_sync": ([P], C.c_int),
             "ff_set_exchange": ([P, i32, i32, P, P, C.c_double], C.c_int),
             "ff_set_exchange_multicast": ([P, P], C.c_int),
+            "ff_set_exchange_push": ([P, i32, P], C.c_int),
             "ff_set_grid_limit": ([P, i32], C.c_int),
             "ff_write_state_async": ([P, i32, i64, i64, P], C.c_int),
             "ff_read_image_async": ([P, P], C.c_int),

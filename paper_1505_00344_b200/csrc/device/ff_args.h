@@ -74,6 +74,11 @@ struct FFStepArgs {
   ff_u32* colour_img;   // null = off
   float col_lo[3], col_s[3];
   int static_rounds;    // tile rounds assigned statically (block b: b, b + grid, ...) before the counter
+  // fused (push) image exchange (ff_set_exchange_push; read only by FF_PUSH builds): every reduction
+  // into the image goes to each of push_img[0 .. push_n) (FF_PUSH 1: every rank's image, as mapped in
+  // this process) or to the images' NVLS multicast address push_img[0] (FF_PUSH 2)
+  ff_u32* push_img[FF_MAX_PEERS_];
+  int push_n;
   float bound_lo[FF_MAX_DIM_], bound_hi[FF_MAX_DIM_];
   FFGroup g[FF_MAX_GROUPS_];
   // step constants of the components with a factored uniform scale s (FF_SSLOT[d] in the generated
@@ -98,6 +103,7 @@ struct FFXchgArgs {
   ff_u64 timeout_ns;            // bound on every wait (a missing peer cannot hang the GPU)
   int rank, world;
   ff_u32* mc;                   // NVLS multicast address of the images (same layout) or null
+  int phase;                    // ff_xbarrier: 1 = before a pushing launch (2 seq + 1), 2 = after it
 };
 
 // Lifted-parameter readback (ff_read_lifted): the swept value of particles [local, local + count) of

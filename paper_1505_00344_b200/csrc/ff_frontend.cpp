@@ -1117,7 +1117,7 @@ std::vector<float> eval_program(const UProgram& prog, const std::vector<float>& 
 }
 
 std::string emit_source(const System& s, int sweep_param, int kernel_select, UProgram* prog, bool balance,
-                        bool long_launch, bool thread_redraw) {
+                        bool long_launch, bool thread_redraw, int push) {
   if (sweep_param < -1 || sweep_param >= (int)s.param_names.size())
     throw Error(FF_ERR_INVALID_ARG, "sweep parameter index out of range");
   // pass 1: lower once to find exponentials sharing an affine argument c w + d
@@ -1408,6 +1408,8 @@ std::string emit_source(const System& s, int sweep_param, int kernel_select, UPr
   // reset redraw of the 4-particles-per-thread kernel: per thread for launches of >= 50 steps (nearly
   // every reset-prone particle resets each launch), warp-cooperative otherwise (ff_reset)
   pre << "#define FF_THREAD_REDRAW " << (thread_redraw ? 1 : 0) << "\n";
+  // fused (push) image exchange: where the histogram's reductions go (ff_img_add; 0 = the bound image)
+  if (push) pre << "#define FF_PUSH " << push << "\n";
 
   std::string tmpl(kDeviceTemplate);
   const std::string marker = "#include_generated_rhs";

@@ -85,8 +85,10 @@ std::vector<float> eval_program(const UProgram& prog, const std::vector<float>& 
 // launches too small to fill the GPU use balance = false: the polynomial lengthens the RK4 chain).
 // long_launch: register budget of the packed 128-thread kernel for launches of many steps (systems
 // of <= 4 variables: 40 registers instead of full occupancy's 32).
+// push: the fused image exchange's reductions (FF_PUSH in ff_device.cuh: 0 none, 1 every rank's image
+// over peer memory, 2 the NVLS multicast address; ff_set_exchange_push).
 std::string emit_source(const System& s, int sweep_param, int kernel_select = 255, UProgram* prog = nullptr,
-                        bool balance = true, bool long_launch = false, bool thread_redraw = false);
+                        bool balance = true, bool long_launch = false, bool thread_redraw = false, int push = 0);
 
 // NVRTC: source -> sm_100a CUBIN (throws Error(FF_ERR_COMPILE) with the log).
 std::vector<char> compile_cubin(const std::string& source, const std::string& name);

@@ -21,7 +21,7 @@
 static_assert(sizeof(FFGroup) == 120, "FFGroup layout");
 static_assert(FF_MAX_SCALED_ == FF_MAX_SCALED, "scaled-component table size");
 static_assert(FF_MAX_DERIVED_ == FF_MAX_DERIVED, "derived-value table size");
-static_assert(offsetof(FFStepArgs, g) == 768, "FFStepArgs layout");  // (one: in the padding before g)
+static_assert(offsetof(FFStepArgs, g) == 840, "FFStepArgs layout");
 static_assert(FF_MAX_PEERS_ == FF_MAX_PEERS, "peer table size");
 static_assert(FF_MAX_DIM_ == FF_MAX_DIM, "bounds table size");
 static_assert(FF_MAX_GROUPS_ == FF_MAX_GROUPS, "group table size");
@@ -47,12 +47,14 @@ struct Module {
   // step kernels by (ppt, tpb): 0 p1t128, 1 p1t256, 2 p1t512, 3 p2t128, 4 p2t256, 5 p4t128;
   // +6 = the same with position-linear colour compiled in (ff_project_colour)
   cudaKernel_t exchange = nullptr;  // (in base_lib)
+  cudaKernel_t xbarrier = nullptr;  // (in base_lib) barrier of the fused (push) exchange
   // [variant][id]: variant = balanced + 2 long; balanced = exponentials shared with the FMA pipe,
   // long = the register budget for launches of many steps (emit_source balance, long_launch)
   // (+4: the per-thread reset redraw of the 4-particle kernel for launches of >= 50 steps)
-  cudaLibrary_t step_lib[8][12] = {};
-  cudaKernel_t step[8][12] = {};
-  int occ[8][12] = {};
+  // (+8 push: the fused exchange's reductions, 1 = to every rank's image, 2 = to the multicast address)
+  cudaLibrary_t step_lib[24][12] = {};
+  cudaKernel_t step[24][12] = {};
+  int occ[24][12] = {};
 };
 
 constexpr int kNumStep = 6;
@@ -126,6 +128,8 @@ struct ff_ctx {
   uint64_t xbar = 0, xseq = 0, xtimeout_ns = 0;
   bool xused = false;
   uint32_t* xmc = nullptr;   // NVLS multicast address of the images (ff_set_exchange_multicast)
+  int xpush = 0;             // ff_set_exchange_push: 0 sum pass, 1 peer reductions, 2 multicast reductions
+  uint32_t* xpush_mc = nullptr;
   bool captured = false;     // a launch was captured into a CUDA graph: reset the tile counter per launch
 
   ~ff_ctx() {
@@ -171,9 +175,10 @@ struct ff_ctx {
     ck(cudaStreamSynchronize(stream), "cudaStreamSynchronize");  // host buffers go out of scope
   }
 
-  cudaLibrary_t load(int sweep, int ksel, bool bal = true, bool long_launch = false, bool thread_redraw = false) {
-    std::vector<char> cubin = ff::compile_cubin(ff::emit_source(sys, sweep, ksel, nullptr, bal, long_launch, thread_redraw),
-                                                "fireflies_system.cu");
+  cudaLibrary_t load(int sweep, int ksel, bool bal = true, bool long_launch = false, bool thread_redraw = false,
+                     int push = 0) {
+    std::vector<char> cubin = ff::compile_cubin(
+        ff::emit_source(sys, sweep, ksel, nullptr, bal, long_launch, thread_redraw, push), "fireflies_system.cu");
     cudaLibrary_t lib = nullptr;
     ck(cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0), "cudaLibraryLoadData");
     return lib;
@@ -188,14 +193,16 @@ struct ff_ctx {
     ck(cudaLibraryGetKernel(&m.init, m.base_lib, "ff_init"), "cudaLibraryGetKernel(ff_init)");
     ck(cudaLibraryGetKernel(&m.render, m.base_lib, "ff_render"), "cudaLibraryGetKernel(ff_render)");
     ck(cudaLibraryGetKernel(&m.exchange, m.base_lib, "ff_exchange"), "cudaLibraryGetKernel(ff_exchange)");
+    ck(cudaLibraryGetKernel(&m.xbarrier, m.base_lib, "ff_xbarrier"), "cudaLibraryGetKernel(ff_xbarrier)");
     ck(cudaLibraryGetKernel(&m.lifted, m.base_lib, "ff_lifted"), "cudaLibraryGetKernel(ff_lifted)");
     return modules.emplace(sweep, m).first->second;
   }
 
-  // step kernel `id` (0-11) of variant v (balanced + 2 long), compiled at its first launch
+  // step kernel `id` (0-11) of variant v (balanced + 2 long + 4 thread redraw + 8 push), compiled at
+  // its first launch
   cudaKernel_t step_kernel(Module& m, int sweep, int id, int v) {
     if (!m.step[v][id]) {
-      m.step_lib[v][id] = load(sweep, id, (v & 1) != 0, (v & 2) != 0, (v & 4) != 0);
+      m.step_lib[v][id] = load(sweep, id, (v & 1) != 0, (v & 2) != 0, (v & 4) != 0, v >> 3);
       const std::string name = std::string(kStepNames[id % kNumStep]) + (id >= kNumStep ? "_c" : "");
       ck(cudaLibraryGetKernel(&m.step[v][id], m.step_lib[v][id], name.c_str()), "cudaLibraryGetKernel(ff_step)");
       int occ = 0;
@@ -418,15 +425,27 @@ struct ff_ctx {
       const std::vector<float> q = ff::eval_program(uprogram(sweep_param, bal), params);
       for (size_t k = 0; k < q.size(); ++k) a.q[k] = q[k];
     }
+    // fused (push) exchange: the histogram's reductions go to every rank's image, between two barriers
+    const int push = (xworld > 1 && image) ? xpush : 0;
+    if (push) {
+      a.push_n = push == 2 ? 1 : xworld;
+      for (int p = 0; p < a.push_n; ++p) a.push_img[p] = push == 2 ? xpush_mc : ximg[p];
+    }
     if (ntiles == 0) {
-      if (xworld > 1) launch_exchange(m);  // this rank has no particles; its peers still wait for it
+      if (push) {                           // this rank has no particles; its peers still wait for it
+        launch_xbarrier(m, 1);
+        launch_xbarrier(m, 2);
+        ++xseq;
+      } else if (xworld > 1) {
+        launch_exchange(m);
+      }
       return;
     }
     // position-linear colour: 3 extra per-block table planes in dynamic shared memory
     const bool colour = image && colour_img;
     const size_t dyn_smem = colour ? 3 * 1024 * sizeof(uint32_t) : 0;
     const int kid = si + (colour ? kNumStep : 0);
-    const int var = variant_for(bal, kid, n_steps);
+    const int var = variant_for(bal, kid, n_steps) + 8 * push;
     if (capturing && !m.step[var][kid])
       throw ff::Error(FF_ERR_STATE, "graph capture: this launch's kernel is not compiled yet -- run the frame once "
                                     "before capturing it");
@@ -448,12 +467,36 @@ struct ff_ctx {
     const int64_t ns = (n_steps <= 2 && sys.dim <= 8 && ntiles / grid >= 2) ? ntiles / grid - 1 : 0;
     a.static_rounds = (int)ns;
     void* args[] = {&a};
+    if (push) launch_xbarrier(m, 1);
     ck(cudaLaunchKernel((const void*)kern, dim3(grid), dim3(t), args, dyn_smem, stream), "launch ff_step");
     // static rounds first (ff_step_body), then each block fetches dynamic tiles until it sees one past
     // the end: the counter advances by the dynamic tiles + grid
     tile_base += (uint64_t)(ntiles - ns * (int64_t)grid) + grid;
     ++launches;
-    if (xworld > 1 && image) launch_exchange(m);  // (one rank: its image already is the sum)
+    if (push) {
+      launch_xbarrier(m, 2);
+      ++xseq;
+    } else if (xworld > 1 && image) {
+      launch_exchange(m);  // (one rank: its image already is the sum)
+    }
+  }
+
+  // a barrier of the fused (push) exchange (ff_xbarrier in ff_device.cuh): phase 1 before the pushing
+  // launch, 2 after it; barrier values 2 xseq + phase on the exchange's signal words
+  void launch_xbarrier(Module& m, int phase) {
+    FFXchgArgs x;
+    std::memset(&x, 0, sizeof x);
+    for (int p = 0; p < xworld; ++p) x.sig[p] = reinterpret_cast<ff_u64*>(xsig[p]);
+    x.sync = reinterpret_cast<ff_u64*>(tile_ctr) + 16;
+    x.seq = xseq;
+    x.timeout_ns = xtimeout_ns;
+    x.rank = xrank;
+    x.world = xworld;
+    x.phase = phase;
+    void* args[] = {&x};
+    ck(cudaLaunchKernel((const void*)m.xbarrier, dim3(1), dim3(32), args, 0, stream), "launch ff_xbarrier");
+    xused = true;
+    ++launches;
   }
 
   // the image exchange after a binning launch (ff_set_exchange; ff_device.cuh "image exchange")
@@ -868,6 +911,8 @@ ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view
   ctx->image = image;
   ctx->xworld = 0;  // (re)binding an image ends an exchange (ff_set_exchange again)
   ctx->xmc = nullptr;
+  ctx->xpush = 0;
+  ctx->xpush_mc = nullptr;
   if (!ctx->groups.empty()) ctx->launch_step(0, 0.0f);
   FF_CATCH
 }
@@ -1047,7 +1092,8 @@ ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* pee
   if (world == 0) {
     ctx->xworld = 0;
     ctx->xmc = nullptr;
-    ctx->xmc = nullptr;
+    ctx->xpush = 0;
+    ctx->xpush_mc = nullptr;
     return FF_OK;
   }
   need(world >= 1 && world <= FF_MAX_PEERS && rank >= 0 && rank < world, FF_ERR_INVALID_ARG,
@@ -1088,6 +1134,8 @@ ff_status ff_set_exchange(ff_ctx* ctx, int rank, int world, uint32_t* const* pee
   ctx->xseq = 0;
   ctx->xtimeout_ns = (uint64_t)(timeout_ms * 1e6);
   ctx->xmc = nullptr;
+  ctx->xpush = 0;
+  ctx->xpush_mc = nullptr;
   FF_CATCH
 }
 
@@ -1097,6 +1145,38 @@ ff_status ff_set_exchange_multicast(ff_ctx* ctx, uint32_t* mc_image) {
   need(mc_image == nullptr || ctx->xworld >= 1, FF_ERR_STATE, "set up the exchange with ff_set_exchange first");
   need(((uintptr_t)mc_image & 15) == 0, FF_ERR_INVALID_ARG, "the multicast address must be 16-byte aligned");
   ctx->xmc = mc_image;
+  FF_CATCH
+}
+
+ff_status ff_set_exchange_push(ff_ctx* ctx, int on, uint32_t* mc_image) {
+  FF_TRY
+  need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
+  need(on == 0 || on == 1, FF_ERR_INVALID_ARG, "on must be 0 or 1");
+  need(((uintptr_t)mc_image & 15) == 0, FF_ERR_INVALID_ARG, "the multicast address must be 16-byte aligned");
+  if (!on) {
+    ctx->xpush = 0;
+    ctx->xpush_mc = nullptr;
+    return FF_OK;
+  }
+  need(ctx->xworld >= 1, FF_ERR_STATE, "set up the exchange with ff_set_exchange first");
+  const int push = mc_image ? 2 : 1;
+  // compile / load the pushing step kernels and the barrier now (as ff_set_exchange does for its
+  // kernels): no NVRTC compile or lazy module load between the ranks' first pushing launches, while a
+  // peer's barrier may already be spinning on the device
+  Module& m = ctx->module(ctx->sweep_param);
+  if (ctx->xworld > 1) {
+    for (int64_t n : {1, 10, 100}) {
+      int pp, tt;
+      ctx->default_launch(pp, tt, n);
+      const int id = step_index(pp, tt);
+      for (int bal = 0; bal < 2; ++bal)
+        ctx->step_kernel(m, ctx->sweep_param, id, ctx->variant_for(bal != 0, id, n) + 8 * push);
+    }
+  }
+  cudaFuncAttributes fa;
+  ck(cudaFuncGetAttributes(&fa, (const void*)m.xbarrier), "cudaFuncGetAttributes(ff_xbarrier)");
+  ctx->xpush = push;
+  ctx->xpush_mc = mc_image;
   FF_CATCH
 }
 

@@ -1,7 +1,9 @@
 """Multi-GPU plumbing: one process per GPU, particles sharded contiguously per group
 (ff_set_shard / ff_shard_range), and the path's one exchange step -- the per-frame sum of the
 int32 density images -- either fused into the step launch over NVLink peer memory
-(bind_exchanged_image -> ff_set_exchange; torch symmetric memory only maps the buffers) or as a
+(bind_exchanged_image -> ff_set_exchange: a sum pass after the launch, or with push=True the
+histogram's own reductions sent to every rank's image, ff_set_exchange_push; torch symmetric memory
+only maps the buffers) or as a
 torch.distributed all-reduce (reduce_image: NCCL over NVLink/NVSwitch on GPUs, gloo on CPU in the
 tests). Parameters changed on rank 0 are broadcast so every shard integrates the same system
 (PAPER.md:242)."""
@@ -92,14 +94,17 @@ def _map_ipc(buf, group):
 
 
 def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=1000.0, mapping="auto",
-                         multicast=False):
+                         multicast=False, push=False):
     """Bind a peer-accessible image to `ctx` and turn on the library's image exchange: from now on
     every binning ff_step of every rank is followed, on its stream, by the sum of the images over all
     ranks (ff_set_exchange; no separate collective). Collective over `group` (default: the world);
     returns the bound image tensor [C][H][W] (int32, zeroed). mapping: "symmetric" (torch symmetric
     memory), "ipc" (CUDA IPC handles), "auto" (symmetric, else IPC). multicast=True additionally binds
     the NVLS multicast mapping of the images (torch symmetric memory's multicast_ptr;
-    ff_set_exchange_multicast) and raises if the system offers none."""
+    ff_set_exchange_multicast) and raises if the system offers none. push=True selects the fused
+    (push) exchange instead of the sum pass: the histogram's reductions go straight to every rank's
+    image (over peer memory, or with multicast=True as multimem.red through the multicast mapping;
+    ff_set_exchange_push) between two barriers per launch; zero the image on every rank per frame."""
     words, sig_off, total = exchange_layout(C_, H, W)
     if not dist.is_initialized() or dist.get_world_size(group) == 1:   # one rank: its own tables
         buf = torch.zeros(total, dtype=torch.int32, device=ctx.device)
@@ -109,6 +114,8 @@ def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=100
         torch.cuda.synchronize(ctx.device)
         imgs, sigs = peer_tables([buf.data_ptr()], C_, H, W)
         ctx.set_exchange(0, 1, imgs, sigs, timeout_ms)
+        if push:
+            ctx.set_exchange_push(True)
         ctx._symm = (buf,)
         return image
     group = group if group is not None else dist.group.WORLD
@@ -143,6 +150,11 @@ def bind_exchanged_image(ctx, axes, view, W, H, C_=1, group=None, timeout_ms=100
         if not int(ok.item()):
             ctx.set_exchange(0, 0)
             raise RuntimeError("no NVLS multicast mapping for this group (symmetric memory multicast_ptr = 0)")
-        ctx.set_exchange_multicast(mc)
+        if push:
+            ctx.set_exchange_push(True, mc)
+        else:
+            ctx.set_exchange_multicast(mc)
+    elif push:
+        ctx.set_exchange_push(True)
     ctx._symm = (buf, keep)                            # keep the mappings alive with the context
     return image

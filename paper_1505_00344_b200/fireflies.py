@@ -206,6 +206,12 @@ def ff_set_exchange_multicast(ctx, mc_image_ptr: int):
     check(lib().ff_set_exchange_multicast(ctx, C.c_void_p(int(mc_image_ptr)) if mc_image_ptr else None))
 
 
+def ff_set_exchange_push(ctx, on: bool, mc_image_ptr: int = 0):
+    """Fused (push) exchange: the histogram's reductions go to every rank's image (mc_image_ptr = 0:
+    red.add per peer image; else multimem.red.add through the multicast address)."""
+    check(lib().ff_set_exchange_push(ctx, 1 if on else 0, C.c_void_p(int(mc_image_ptr)) if mc_image_ptr else None))
+
+
 def ff_set_grid_limit(ctx, max_blocks: int):
     check(lib().ff_set_grid_limit(ctx, max_blocks))
 
@@ -359,6 +365,9 @@ class Context:
 
     def set_exchange_multicast(self, mc_image_ptr):
         ff_set_exchange_multicast(self.ctx, mc_image_ptr)
+
+    def set_exchange_push(self, on=True, mc_image_ptr=0):
+        ff_set_exchange_push(self.ctx, on, mc_image_ptr)
 
     def set_grid_limit(self, max_blocks):
         ff_set_grid_limit(self.ctx, max_blocks)

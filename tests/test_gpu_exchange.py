@@ -54,6 +54,7 @@ def exchanged_ranks(world, image_shape, axes, view, grid_limit=16, timeout_ms=20
     torch.cuda.synchronize()
     for r, (ctx, img) in enumerate(ranks):
         ctx.set_exchange(r, world, [i.data_ptr() for _, i in ranks], [s.data_ptr() for s in sigs], timeout_ms)
+        ctx._keep_signals = sigs    # the signal words must outlive the contexts' exchanged launches
     return ranks, streams, sigs
 
 

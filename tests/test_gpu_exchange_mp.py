@@ -1,6 +1,7 @@
 """The image exchange across PROCESSES (one GPU, two ranks): dist.bind_exchanged_image maps the
 peers' images with CUDA IPC (torch symmetric memory refuses two ranks on one device; across GPUs the
-same code maps NVLink peer memory), ff_set_exchange sums them after every binning launch. Each rank's
+same code maps NVLink peer memory), ff_set_exchange sums them after every binning launch (or, with
+ff_set_exchange_push, the histogram's reductions go to both images). Each rank's
 image must equal the oracle histogram of all particles (bin-only frame) and the unsharded image of a
 single-process run (integrating frames), bit-exact."""
 import os
@@ -29,7 +30,7 @@ def make_ctx(rank, world):
     return ctx
 
 
-def worker(rank, world, port, out):
+def worker(rank, world, port, out, push=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     import torch.distributed as dist
     from paper_1505_00344_b200 import dist as ffdist
@@ -37,7 +38,7 @@ def worker(rank, world, port, out):
     dist.init_process_group("gloo")
     ctx = make_ctx(rank, world)
     C_, H, W = SHAPE
-    img = ffdist.bind_exchanged_image(ctx, AXES, VIEW, W, H, C_, timeout_ms=30000.0, mapping="ipc")
+    img = ffdist.bind_exchanged_image(ctx, AXES, VIEW, W, H, C_, timeout_ms=30000.0, mapping="ipc", push=push)
     frames = []
     for n_steps in (0, 4, 7):
         img.zero_()
@@ -57,13 +58,16 @@ def free_port():
         return s.getsockname()[1]
 
 
-def test_two_process_exchange_matches_oracle_and_unsharded_run():
+@pytest.mark.parametrize("push", [False, True])
+def test_two_process_exchange_matches_oracle_and_unsharded_run(push):
+    """push=False: the sum pass after each launch (ff_set_exchange); push=True: the histogram's
+    reductions sent to both processes' images (ff_set_exchange_push, red.add over the IPC mapping)."""
     import torch.multiprocessing as mp
     import oracle as O
     world = 2
     mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
-    mp.spawn(worker, args=(world, free_port(), out), nprocs=world, join=True)
+    mp.spawn(worker, args=(world, free_port(), out, push), nprocs=world, join=True)
     C_, H, W = SHAPE
     want0 = np.zeros(SHAPE, np.uint32)
     for n, seed, _, colour in GROUPS:

@@ -1,6 +1,6 @@
 """The NVLS variant of the image exchange (ff_set_exchange_multicast): two
 processes on two GPUs, images in torch symmetric memory, the sum pass through NVSwitch multicast
-(multimem.ld_reduce + multimem.st). Each rank's image must equal the oracle histogram of all particles
+(multimem.ld_reduce + multimem.st), or the histogram's reductions as multimem.red (push). Each rank's image must equal the oracle histogram of all particles
 (bin-only frame) and the unsharded single-process image (integrating frames), bit-exact. Needs >= 2
 GPUs on a multicast-capable NVSwitch system: skipped otherwise (the one-GPU boxes of this run refuse
 multicast objects, tools/probe_mc.py)."""
@@ -19,7 +19,7 @@ if not torch.cuda.is_available() or torch.cuda.device_count() < 2:  # pragma: no
 from test_gpu_exchange_mp import AXES, GROUPS, LO, HI, SHAPE, VIEW, free_port, make_ctx  # noqa: E402
 
 
-def worker(rank, world, port, out):
+def worker(rank, world, port, out, push=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     import torch.distributed as dist
     from paper_1505_00344_b200 import dist as ffdist
@@ -29,7 +29,7 @@ def worker(rank, world, port, out):
     C_, H, W = SHAPE
     try:
         img = ffdist.bind_exchanged_image(ctx, AXES, VIEW, W, H, C_, timeout_ms=30000.0, mapping="symmetric",
-                                          multicast=True)
+                                          multicast=True, push=push)
     except RuntimeError as e:
         out[rank] = f"skip: {e}"
         dist.destroy_process_group()
@@ -47,12 +47,15 @@ def worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_nvls_exchange_matches_oracle_and_unsharded_run():
+@pytest.mark.parametrize("push", [False, True])
+def test_nvls_exchange_matches_oracle_and_unsharded_run(push):
+    """push=False: the sum pass through multimem.ld_reduce / multimem.st; push=True: the histogram's
+    reductions issued once each as multimem.red.add to the multicast address (ff_set_exchange_push)."""
     import torch.multiprocessing as mp
     import oracle as O
     world = 2
     out = mp.get_context("spawn").Manager().dict()
-    mp.spawn(worker, args=(world, free_port(), out), nprocs=world, join=True)
+    mp.spawn(worker, args=(world, free_port(), out, push), nprocs=world, join=True)
     if any(isinstance(out[r], str) for r in range(world)):
         pytest.skip(str(out[0]))
     C_, H, W = SHAPE

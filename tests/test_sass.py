@@ -133,3 +133,41 @@ def test_bench_kernel_p4_loop(tmp_path, monkeypatch):
     res = subprocess.run(["cuobjdump", "-res-usage", str(p)], capture_output=True, text=True).stdout
     m = re.search(r"Function ff_step_p4_t128:\s+REG:(\d+) STACK:(\d+)", res)
     assert m and int(m.group(1)) <= 64 and int(m.group(2)) == 0
+
+
+@pytest.mark.parametrize("push", [0, 1, 2])
+def test_push_exchange_builds(tmp_path, push):
+    """The fused (push) exchange's builds of the bench kernel (ff_set_exchange_push; emitted with
+    FF_PUSH = push, compiled here with nvcc from the generated source): the RK4 loop is untouched
+    (the same 164 packed instructions, no spills, same register budget), and the histogram's
+    reductions are gpu-scope REDs into the bound image (0), system-scope REDs to the peers' images
+    (1), or multimem.red.add to the multicast address (2: PTX multimem.red, which ptxas lowers to a
+    system-scope REDG on the multicast address -- the NVSwitch fans it out)."""
+    src = FF.ff_emit_source(systems.lorenz())
+    unroll = re.search(r"#define FF_UNROLL (\d+)", src).group(1)
+    src = src.replace("#pragma unroll FF_UNROLL", f"#pragma unroll {unroll}")   # (nvcc: literal only)
+    src = src.replace("#define FF_KSEL 255", "#define FF_KSEL 5")
+    src = src.replace("#define FF_MINB_P4 ", "#define FF_MINB_P4 8 //")
+    if push:
+        src = f"#define FF_PUSH {push}\n" + src
+    cu = tmp_path / "k.cu"
+    cu.write_text(src)
+    for kind in ("ptx", "cubin"):
+        subprocess.run(["nvcc", f"-{kind}", "-gencode", "arch=compute_100a,code=sm_100a", "-w", "-o",
+                        str(tmp_path / f"k.{kind}"), str(cu)], check=True, capture_output=True)
+    ptx = (tmp_path / "k.ptx").read_text()
+    n_mm = ptx.count("multimem.red.relaxed.sys.global.add.u32")
+    n_sys = ptx.count("red.relaxed.sys.global.add.u32") - n_mm
+    n_gpu = ptx.count("red.relaxed.gpu.global.add.u32")
+    assert (n_mm > 0, n_sys > 0, n_gpu > 0) == (push == 2, push == 1, push == 0)
+    loops = [c for c in inner_loops(str(tmp_path / "k.cubin"), "ff_step_p4_t128") if c["FFMA2"] >= 80]
+    main = min(loops, key=lambda c: sum(c.values()))
+    assert main["FFMA2"] + main["FMUL2"] + main["FADD2"] == 164
+    assert main["LDL"] == 0 and main["STL"] == 0
+    sass = subprocess.run(["cuobjdump", "-sass", "-fun", "ff_step_p4_t128", str(tmp_path / "k.cubin")],
+                          capture_output=True, text=True).stdout
+    reds = [r for r in re.findall(r"\bREDG?\.\S*", sass) if ".ADD" in r]
+    assert reds and all(("SYS" in r) == (push > 0) for r in reds), set(reds)
+    res = subprocess.run(["cuobjdump", "-res-usage", str(tmp_path / "k.cubin")], capture_output=True, text=True).stdout
+    m = re.search(r"Function ff_step_p4_t128:\s+REG:(\d+) STACK:(\d+)", res)
+    assert m and int(m.group(1)) <= 64 and int(m.group(2)) == 0
