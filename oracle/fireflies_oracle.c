@@ -28,7 +28,10 @@
  *                          (tests/golden/reset_golden.json), inclusive bounds, epochs, uniformity
  *   rhs_stn                pinned by special cases (w = 0 closed form, forward invariance of
  *                          (0,1)^2 per PAPER.md:40); the sigmoid constants themselves are
- *                          unpublished -> "parity unpinned" for their values (reading R6)
+ *                          unpublished (reading R6), their values pinned only against the phase
+ *                          portraits the paper prints (w_ss = 0 / 7.8 / 11 and the
+ *                          Hopf / SNIC order) -- the w_ss = 4.9 limit-cycle pair is not reproduced,
+ *                          so "parity unpinned" for the exact values
  *   philox4x32_10          pinned: Random123 known-answer vectors
  *   ic / sweep / project   pinned: bin-centre placement, edge rules, brute force, golden pixels
  *

@@ -261,6 +261,98 @@ def test_stn_backward_particles_leave():
     assert out.mean() > 0.95
 
 
+def _stn_fixed_points(p):
+    """Fixed points of Eqs. 1-2 in the unit square (Newton from a grid) with their Jacobian
+    eigenvalues (central differences of the oracle's RHS)."""
+    from scipy.optimize import fsolve
+    F = lambda z: np.asarray(O.rhs(O.STN, [z[0], z[1]], p))
+    out = []
+    for a in np.linspace(0.02, 0.98, 13):
+        for b in np.linspace(0.02, 0.98, 13):
+            z, _, ier, _ = fsolve(F, [a, b], full_output=True)
+            if ier == 1 and np.all(np.abs(F(z)) < 1e-11) and np.all((z > 0) & (z < 1)) and \
+                    not any(np.allclose(z, q, atol=1e-7) for q, _ in out):
+                e = 1e-7
+                J = np.array([(F(z + [e, 0]) - F(z - [e, 0])) / (2 * e), (F(z + [0, e]) - F(z - [0, e])) / (2 * e)]).T
+                out.append((z, np.linalg.eigvals(J)))
+    return out
+
+
+def _stn_forward_orbits(w_ss, n=300, steps=20000):
+    """Per-particle range of x (sampled every 5 steps) over the last 2000 steps of `steps` forward
+    RK4 steps (dt = 0.01) from uniform ICs in (0,1)^2."""
+    rng = np.random.default_rng(33)
+    x = O.rk4(O.STN, rng.uniform(0, 1, (2, n)), stn_p(w_ss=w_ss), 0.01, steps - 2000)
+    lo, hi = x.copy(), x.copy()
+    for _ in range(400):
+        x = O.rk4(O.STN, x, stn_p(w_ss=w_ss), 0.01, 5)
+        lo, hi = np.minimum(lo, x), np.maximum(hi, x)
+    return hi[0] - lo[0], x
+
+
+def test_stn_paper_phase_portraits_at_w0_w78_w11():
+    """The constants of reading R6 (unpublished in the paper) against the phase portraits the paper
+    prints (PAPER.md:47, Fig. 2 caption; :50, :52): w_ss = 0 -- a single, globally stable spiral;
+    w_ss = 7.8 -- an unstable spiral and a (globally attracting) stable limit cycle; w_ss = 11 -- an
+    unstable node, a saddle and a stable node. (At w_ss = 4.9 the paper also shows a pair of limit
+    cycles around the stable spiral; with R6's constants the spiral is stable there but no cycle
+    pair appears -- DESIGN.md R6.)"""
+    fp = _stn_fixed_points(stn_p(w_ss=0.0))
+    assert len(fp) == 1
+    ev = fp[0][1]
+    assert np.all(ev.real < 0) and np.all(np.abs(ev.imag) > 0.1)            # stable spiral
+    amp, x = _stn_forward_orbits(0.0)
+    assert amp.max() < 1e-9 and np.abs(x - fp[0][0][:, None]).max() < 1e-9  # every particle reaches it
+
+    fp = _stn_fixed_points(stn_p(w_ss=7.8))
+    assert len(fp) == 1
+    ev = fp[0][1]
+    assert np.all(ev.real > 0) and np.all(np.abs(ev.imag) > 0.1)            # unstable spiral
+    amp, _ = _stn_forward_orbits(7.8)
+    assert amp.min() > 0.5 and amp.max() - amp.min() < 2e-3                 # one stable cycle for all
+
+    fp = _stn_fixed_points(stn_p(w_ss=11.0))
+    assert len(fp) == 3
+    kinds = sorted((int(np.sum(e.real > 0)), bool(np.all(np.abs(e.imag) < 1e-12))) for _, e in fp)
+    assert kinds == [(0, True), (1, True), (2, True)]    # stable node, saddle, unstable node
+    amp, _ = _stn_forward_orbits(11.0)
+    assert amp.max() < 1e-6                              # no oscillation left (after the SNIC)
+
+
+def test_stn_bifurcation_order_along_w_ss():
+    """PAPER.md:52 (and Fig. 3 caption): increasing w_ss, the fixed point loses stability in an
+    Andronov-Hopf bifurcation, then a saddle-node on the invariant circle leaves a new stable fixed
+    point -- the Hopf lies between the paper's w_ss = 4.9 (stable spiral) and 7.8 (unstable spiral),
+    the SNIC between 7.8 (a cycle) and 11 (three fixed points), and the period grows as the SNIC
+    approaches ("bunching up", PAPER.md:52)."""
+    from scipy.optimize import brentq
+
+    def re_max(w):
+        fp = _stn_fixed_points(stn_p(w_ss=w))
+        assert len(fp) == 1
+        return fp[0][1].real.max()
+    assert re_max(4.9) < 0 < re_max(7.8)
+    w_h = brentq(re_max, 4.9, 7.8, xtol=1e-6)
+    assert 4.9 < w_h < 7.8
+    n_fp = {w: len(_stn_fixed_points(stn_p(w_ss=w))) for w in (7.8, 9.0, 10.0, 10.5, 11.0)}
+    first3 = min(w for w, k in n_fp.items() if k == 3)
+    assert all(k == 1 for w, k in n_fp.items() if w < first3) and all(k == 3 for w, k in n_fp.items() if w >= first3)
+    assert 7.8 < first3 <= 11.0
+
+    def period(w):   # time between successive upward crossings of the cycle's mean x
+        _, x = _stn_forward_orbits(w, n=1, steps=20000)
+        p = stn_p(w_ss=w)
+        xs, c = [], None
+        for _ in range(6000):
+            x = O.rk4(O.STN, x, p, 0.01, 1)
+            xs.append(x[0, 0])
+        xs = np.array(xs)
+        m = 0.5 * (xs.min() + xs.max())
+        up = np.nonzero((xs[:-1] < m) & (xs[1:] >= m))[0]
+        return np.diff(up).mean() * 0.01
+    assert period(7.8) < period(9.0) < period(10.0)
+
+
 # ----------------------------------------------------------------------------- front-end coverage model
 def test_funcs_model_closed_form_at_origin():
     # sin(0)cos(0) + tanh(0) - (1+0)^0.75 + 0.1 pi ; sqrt(1) - log(2) + exp(0) + |0| - 0 ; 0
