@@ -191,7 +191,7 @@ def ff_sync(ctx):
     check(lib().ff_sync(ctx))
 
 
-def ff_set_exchange(ctx, rank: int, world: int, peer_image_ptrs, peer_signal_ptrs, timeout_ms: float = 60000.0):
+def ff_set_exchange(ctx, rank: int, world: int, peer_image_ptrs, peer_signal_ptrs, timeout_ms: float = 1000.0):
     """Fused in-launch image all-reduce over peer memory (world = 0: off). Pointers are ints."""
     if world == 0:
         check(lib().ff_set_exchange(ctx, 0, 0, None, None, 1.0))
@@ -360,7 +360,7 @@ class Context:
         ff_render(self.ctx, colours, intensity, radius_px, out.data_ptr())
         return out
 
-    def set_exchange(self, rank, world, peer_image_ptrs=(), peer_signal_ptrs=(), timeout_ms=60000.0):
+    def set_exchange(self, rank, world, peer_image_ptrs=(), peer_signal_ptrs=(), timeout_ms=1000.0):
         ff_set_exchange(self.ctx, rank, world, peer_image_ptrs, peer_signal_ptrs, timeout_ms)
 
     def set_exchange_multicast(self, mc_image_ptr):
