@@ -234,7 +234,8 @@ def run_ours(args, w, rank, world, device):
     reduce = dist and not fused
 
     def frame():
-        img.zero_()
+        if not args.no_image:   # (integration-only frames have no image to clear)
+            img.zero_()
         ctx.step(S, w["dt"])
         if reduce:
             torch.distributed.all_reduce(img)
@@ -255,7 +256,8 @@ def run_ours(args, w, rank, world, device):
             elif args.flush == "memset":
                 flush.zero_()
             ev[i][0].record(stream)
-            img.zero_()
+            if not args.no_image:
+                img.zero_()
             ev[i][1].record(stream)
             ctx.step(S, w["dt"])
             if reduce:   # the image sum is part of the frame: it ends before the frame's end event

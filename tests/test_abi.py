@@ -129,6 +129,11 @@ def test_null_context_rejected():
     assert L.ff_step(None, 1, ctypes.c_float(0.01)) == _abi.FF_ERR_INVALID_ARG
     assert L.ff_sync(None) == _abi.FF_ERR_INVALID_ARG
     assert b"ctx is NULL" in L.ff_last_error()
+    # the exchange setters (no device needed to reject them)
+    assert L.ff_set_exchange(None, 0, 0, None, None, 1.0) == _abi.FF_ERR_INVALID_ARG
+    assert L.ff_set_exchange_multicast(None, None) == _abi.FF_ERR_INVALID_ARG
+    assert L.ff_set_exchange_push(None, 1, None) == _abi.FF_ERR_INVALID_ARG
+    assert L.ff_set_grid_limit(None, 0) == _abi.FF_ERR_INVALID_ARG
     assert L.ff_destroy(None) == _abi.FF_OK
 
 
