@@ -76,6 +76,26 @@ WORKLOADS = {
 }
 
 
+# The paper's own numbers for this path (Table 1: one RK4 step per particle, averaged
+# over 1000 steps, rendering excluded, FP32, GTX 460 / OpenCL): context for the bench line, not the
+# target (another machine, other particle counts) -- vs_baseline stays null.
+PAPER_TABLE1 = {
+    "lorenz": dict(particles=3_000_000, ms_per_step=3.0, cite="PAPER.md:175"),
+    "stn_gpe": dict(particles=700_000, ms_per_step=1.0, cite="PAPER.md:174"),
+    "hh_ring3": dict(particles=500_000, ms_per_step=22.0, cite="PAPER.md:176"),
+}
+
+
+def paper_context(system):
+    t = PAPER_TABLE1.get(system)
+    if t is None:
+        return None
+    return {"hardware": "NVIDIA GeForce GTX 460 (Fermi), OpenCL, FP32 (PAPER.md:178, :225)",
+            "particles": t["particles"], "ms_per_step": t["ms_per_step"],
+            "particle_steps_per_s": t["particles"] / (t["ms_per_step"] * 1e-3),
+            "fps_budget": "30 frames/s incl. rendering (PAPER.md:182)", "source": t["cite"]}
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -692,6 +712,9 @@ def main():
                                                                      for q in (10, 50, 90)],
             "image_sum_last_frame": r["image_sum"], "wall_s_timed_region": r["t_wall"],
             "build": __import__("paper_1505_00344_b200.fireflies", fromlist=["x"]).ff_build_info()}
+    ctxt = paper_context(w["system"])
+    if ctxt:
+        line["paper_context"] = ctxt
     if world == 1 and not args.no_cpu_baseline:
         n = reference_sample_size(w, r["S"])
         v, dt, threads, n = cpu_oracle_sample(w, n, r["S"])

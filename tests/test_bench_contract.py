@@ -99,3 +99,13 @@ def test_world_size_must_match_gpus():
                           "--warmup", "1", "--config", "stn"], capture_output=True, text=True, timeout=600,
                          cwd=ROOT, env=dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0"))
     assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr
+
+
+def test_paper_context_quotes_table_1():
+    """The bench line quotes the paper's Table 1 number for its system, with the
+    hardware, as context (vs_baseline stays null: other machine, other particle counts)."""
+    import bench
+    assert bench.paper_context("lorenz")["particle_steps_per_s"] == 3_000_000 / 3e-3
+    assert bench.paper_context("stn_gpe")["particle_steps_per_s"] == 700_000 / 1e-3
+    assert bench.paper_context("hh_ring3")["particle_steps_per_s"] == 500_000 / 22e-3
+    assert all(bench.paper_context(w["system"]) for w in bench.WORKLOADS.values())
