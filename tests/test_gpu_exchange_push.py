@@ -200,3 +200,48 @@ def test_push_off_returns_to_the_sum_pass_and_argument_errors():
     with pytest.raises(FFError) as e:
         lone.set_exchange_push(True)    # no exchange set
     assert e.value.status == FF_ERR_STATE
+
+
+@pytest.mark.parametrize("push", [False, True])
+def test_exchange_full_size_bench_launch(push):
+    """configs[1] at full size in the bench's launch (2^22 forward + 2^22 backward Lorenz particles, the
+    non-finite reset rule, 3-D 1024^2 x 2 image, S = 100 and S = 1 frames, default kernel choice and
+    full grids) sharded over two ranks as contexts on one GPU: after each frame both ranks' images
+    equal the unsharded run's image bit for bit, for the sum-pass exchange and for the push exchange."""
+    from paper_1505_00344_b200.fireflies import ff_set_stream
+    n = 1 << 22
+    sizes = [(n, 2, 1, 0), (n, 3, -1, 1)]
+    axes, shape, M = [0, 1, 2], (2, 1024, 1024), views.lorenz_camera()
+    world = 2
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    ranks = []
+    for r in range(world):
+        ctx = FF.Context(systems.lorenz(), [k for k, _, _, _ in sizes], rank=r, world=world)
+        ff_set_stream(ctx.ctx, streams[r].cuda_stream)
+        ctx.stream = streams[r]
+        for k, seed, d, colour in sizes:
+            ctx.init_group(LZ_LO, LZ_HI, k, d, colour, seed)
+        ctx.set_reset(True, None, None, 0.0)
+        img = torch.zeros(shape, dtype=torch.int32, device="cuda")
+        ctx.project(axes, M, shape[2], shape[1], shape[0], image=img)
+        ranks.append((ctx, img))
+    sigs = [torch.zeros(8, dtype=torch.int64, device="cuda") for _ in range(world)]
+    torch.cuda.synchronize()
+    for r, (ctx, _) in enumerate(ranks):
+        ctx.set_exchange(r, world, [i.data_ptr() for _, i in ranks], [s.data_ptr() for s in sigs], 20000.0)
+        if push:
+            ctx.set_exchange_push(True)
+        ctx._keep_signals = sigs
+    single = FF.Context(systems.lorenz(), [k for k, _, _, _ in sizes])
+    for k, seed, d, colour in sizes:
+        single.init_group(LZ_LO, LZ_HI, k, d, colour, seed)
+    single.set_reset(True, None, None, 0.0)
+    simg = single.project(axes, M, shape[2], shape[1], shape[0])
+    for S in (100, 1, 100):
+        frame(ranks, streams, S)
+        simg.zero_()
+        single.step(S, 0.01)
+        want = single.read_image()
+        assert want.sum() > (1 << 22)          # both groups binned (the reset keeps the backward one in view)
+        for _, img in ranks:
+            assert np.array_equal(img.cpu().numpy().view(np.uint32), want)
