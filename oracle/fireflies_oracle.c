@@ -20,8 +20,10 @@
  *                          onset of repetitive firing ~6.25, the vtrap series
  *                          branch (alpha_m(25) = 1, alpha_n(10) = 0.1, series vs expm1 within its
  *                          truncation term, continuity at |u| = 0.1; reading R10); the synapse
- *                          constants tau_r, tau_d, sigma, theta are unpublished
- *                          -> "parity unpinned" for their values (reading R8)
+ *                          constants tau_r, tau_d, sigma, theta are unpublished,
+ *                          pinned only against PAPER.md:156-158's synchrony and two-spiking cycles
+ *                          (the 1-3-2 sequence cycle of :160 is not reproduced) -> "parity
+ *                          unpinned" for their values (reading R8)
  *   rhs_funcs              pinned: closed forms at the origin and at 3 points where every term
  *                          is non-zero (Python math, double)
  *   reset / lifted values  pinned: an independent Python Philox4x32-10 golden

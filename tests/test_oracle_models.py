@@ -192,6 +192,42 @@ def test_hh_ring_synchronises():
     assert np.mean(worst < 5.0) > 0.5
 
 
+def test_hh_ring_two_spiking_one_silent_cycles():
+    """PAPER.md:158 against reading R8's (unpublished) synapse constants: besides the synchronous
+    state, random initial conditions settle on three limit cycles where two neurons spike and the
+    third is silent -- one per silent neuron -- and in each the pre-synaptic neuron fires first,
+    followed by the post-synaptic one, followed by a pause. (PAPER.md:160's small-basin cycle with all
+    three firing in the order 1, 3, 2 is not reproduced: with R8's constants the three-neuron
+    sequence cycle runs 1, 2, 3, with the coupling -- DESIGN.md R8.)"""
+    rng = np.random.default_rng(22)
+    n = 256
+    x0 = np.vstack([np.vstack([rng.uniform(-20, 100, n), rng.uniform(0, 1, (4, n))]) for _ in range(3)])
+    p = hh_p(3)
+    x = O.rk4(O.HH, x0, p, 0.01, 40000)                     # 400 ms
+    prev = x[0::5].copy()
+    times = [[[] for _ in range(n)] for _ in range(3)]
+    for k in range(1000):                                    # the next 100 ms, spike = V up through 20 mV
+        x = O.rk4(O.HH, x, p, 0.01, 10)
+        V = x[0::5]
+        for i, j in zip(*np.nonzero((prev < 20) & (V >= 20))):
+            times[i][j].append((k + 1) * 0.1)
+        prev = V.copy()
+    seen = set()
+    for j in range(n):
+        firing = [len(times[i][j]) >= 4 for i in range(3)]
+        silent = [len(times[i][j]) == 0 for i in range(3)]
+        if sum(firing) != 2 or sum(silent) != 1:
+            continue
+        q = silent.index(True)                 # silent neuron; (q+1) receives from q (reading R9)
+        pre, post = (q + 1) % 3, (q + 2) % 3   # post receives from pre
+        tp, tq = np.array(times[pre][j]), np.array(times[post][j])
+        lag = [tq[tq > t][0] - t for t in tp[:-1] if np.any(tq > t)]       # pre -> next post spike
+        back = [tp[tp > t][0] - t for t in tq[:-1] if np.any(tp > t)]      # post -> next pre spike
+        assert np.mean(lag) < np.mean(back), (j, q)          # pre fires first, then post, then a pause
+        seen.add(q)
+    assert seen == {0, 1, 2}
+
+
 # ----------------------------------------------------------------------------- STN-GPe
 STN_DEFAULTS = dict(w_ss=0.0, w_gs=8.971, w_sg=15.168, w_gg=8.502, I=2.216, tau_s=1.0, tau_g=2.77,
                     a_s=2.891, theta_s=2.049, a_g=1.826, theta_g=2.032)
