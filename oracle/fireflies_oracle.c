@@ -15,7 +15,9 @@
  * What is pinned (tests/test_oracle_*.py) and what is not -- see DESIGN.md "Oracle":
  *   rk4 (all models)       pinned: closed forms (linear, harmonic), order-4 convergence,
  *                          round trip, fixed points
- *   rhs_lorenz             pinned: PAPER.md:87-93 landmarks, analytic fixed points, rhs(1,1,1)
+ *   rhs_lorenz             pinned: PAPER.md:87-93 landmarks, analytic fixed points, rhs(1,1,1),
+ *                          the homoclinic crossing at r ~ 13.926, chaos at r = 28 and
+ *                          the regular window at r ~ 92 by Lyapunov exponents
  *   rhs_hh                 pinned: textbook m,h,n steady states, rest 0 mV,
  *                          onset of repetitive firing ~6.25, the vtrap series
  *                          branch (alpha_m(25) = 1, alpha_n(10) = 0.1, series vs expm1 within its

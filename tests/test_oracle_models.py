@@ -98,6 +98,50 @@ def hh_p(n, **kw):
     return np.array([d[k] for k in O.hh_param_names(n)])
 
 
+def test_lorenz_homoclinic_explosion_near_13_9():
+    """'At r ~ 13.926 a homoclinic bifurcation occurs ... beyond the bifurcation the
+    separatrices have crossed over': below it the origin's outgoing separatrix spirals into the fixed
+    point on its own side, above it into the one on the opposite side (the strange
+    attractor's appearance at r ~ 13.9 in the bifurcation diagram)."""
+    ends = {}
+    for r in (13.85, 13.9, 13.95, 14.0):
+        p = np.array([10.0, r, 8.0 / 3.0])
+        lam = (-11.0 + np.sqrt(81.0 + 40.0 * r)) / 2.0          # unstable eigenvalue of the origin
+        v = np.array([1.0, (lam + 10.0) / 10.0, 0.0])
+        x = O.rk4(O.LORENZ, (1e-6 * v / np.linalg.norm(v))[:, None], p, 0.001, 200000)
+        c = np.sqrt(8.0 / 3.0 * (r - 1.0))
+        assert np.abs(np.abs(x[:2, 0]) - c).max() < 1e-6 and abs(x[2, 0] - (r - 1.0)) < 1e-6   # settled on C+-
+        ends[r] = np.sign(x[0, 0])
+    assert ends[13.85] == ends[13.9] == 1.0 and ends[13.95] == ends[14.0] == -1.0
+
+
+def _lorenz_lyapunov(r, n=3000, every=10, dt=0.01):
+    """Largest Lyapunov exponent (two trajectories, renormalised every `every` steps)."""
+    p = np.array([10.0, r, 8.0 / 3.0])
+    x = O.rk4(O.LORENZ, np.array([[1.0], [1.0], [20.0]]), p, dt, 5000)
+    y = x.copy()
+    y[0, 0] += 1e-8
+    s = 0.0
+    for _ in range(n):
+        x = O.rk4(O.LORENZ, x, p, dt, every)
+        y = O.rk4(O.LORENZ, y, p, dt, every)
+        d = np.linalg.norm(y - x)
+        s += np.log(d / 1e-8)
+        y = x + (y - x) * (1e-8 / d)
+    return s / (n * every * dt)
+
+
+def test_lorenz_chaos_and_the_periodic_window_near_92():
+    """PAPER.md:95, :100 (Fig. 4): 'small windows of parameter values where the dynamics become
+    regular ... for example at r = 92': the largest Lyapunov exponent is ~0.91 at r = 28 (textbook 0.906), ~0 inside the
+    window (r = 92.5, 93: a stable periodic orbit) and > 1 on both sides of it (r = 90, 95)."""
+    assert 0.85 < _lorenz_lyapunov(28.0) < 0.97
+    for r in (92.5, 93.0):
+        assert abs(_lorenz_lyapunov(r)) < 0.03, r
+    for r in (90.0, 95.0):
+        assert _lorenz_lyapunov(r) > 1.0, r
+
+
 def test_hh_gate_steady_states_textbook():
     # Textbook HH gate values at rest (V = 0): m 0.0529, h 0.5961, n 0.3177 (SPEC.md:459).
     gold = json.load(open(os.path.join(GOLD, "paper_values.json")))["hh"]["textbook_gates_at_rest"]
