@@ -362,7 +362,7 @@ def run_ours(args, w, rank, world, device):
                        "pinned host); two contexts on two streams alternate frames so copy-in, integration "
                        "and copy-out of consecutive frames overlap"}
         ctx2.close()
-    im_sum = int(img.sum().item())
+    im_sum = 0 if args.no_image else int(img.sum().item())   # (no image bound: nothing binned)
     ctx.close()
     sweep_idx = -1
     if "sweep" in w:
