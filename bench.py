@@ -697,7 +697,7 @@ def main():
     roof["traffic"] = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
-        t = json.load(open(prof)).get(f"{args.config}_S{r['S']}")
+        t = json.load(open(prof)).get(f"{args.config}_S{r['S']}" + ("_noimage" if args.no_image else ""))
         if t:
             roof["traffic"] = t
     if clocks.get("sm_mhz"):
