@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: ranges cost a branch unless a profiler attaches
+
 #include "device/ff_args.h"
 #include "ff_internal.hpp"
 
@@ -29,6 +31,12 @@ static_assert(FF_MAX_GROUPS_ == FF_MAX_GROUPS, "group table size");
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range around an ABI call (tracing), visible to ncu --nvtx / Nsight timelines
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
@@ -685,6 +693,7 @@ ff_status ff_group_slots(ff_ctx* ctx, int64_t n_global, int64_t* slots) {
 
 ff_status ff_init_group(ff_ctx* ctx, const float* ic_lo, const float* ic_hi, int64_t n_global, int direction,
                         int colour, uint64_t seed, int* group_id) {
+  NvtxRange nvtx("ff_init_group");
   FF_TRY
   need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
   need(ic_lo && ic_hi, FF_ERR_INVALID_ARG, "ic_lo / ic_hi is NULL");
@@ -870,6 +879,7 @@ ff_status ff_sweep_param(ff_ctx* ctx, int group_id, const char* name, float lo, 
 
 ff_status ff_project(ff_ctx* ctx, const int* axes, int n_axes, const float* view, int W, int H, int C,
                      uint32_t* image) {
+  NvtxRange nvtx("ff_project");
   FF_TRY
   need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
   if (!image) {
@@ -942,6 +952,7 @@ ff_status ff_project_colour(ff_ctx* ctx, const float* lo, const float* hi, uint3
 }
 
 ff_status ff_step(ff_ctx* ctx, int64_t n_steps, float dt) {
+  NvtxRange nvtx("ff_step");
   FF_TRY
   need(ctx, FF_ERR_INVALID_ARG, "ctx is NULL");
   need(n_steps >= 0, FF_ERR_INVALID_ARG, "n_steps must be >= 0");
@@ -999,6 +1010,7 @@ ff_status ff_write_state(ff_ctx* ctx, int group_id, int64_t first, int64_t count
 }
 
 ff_status ff_render(ff_ctx* ctx, const float* colours, float intensity, float radius_px, float* dev_rgb) {
+  NvtxRange nvtx("ff_render");
   FF_TRY
   need(ctx && colours && dev_rgb, FF_ERR_INVALID_ARG, "NULL argument");
   need(ctx->image != nullptr, FF_ERR_STATE, "no image bound");
