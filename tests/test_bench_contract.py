@@ -109,3 +109,33 @@ def test_paper_context_quotes_table_1():
     assert bench.paper_context("stn_gpe")["particle_steps_per_s"] == 700_000 / 1e-3
     assert bench.paper_context("hh_ring3")["particle_steps_per_s"] == 500_000 / 22e-3
     assert all(bench.paper_context(w["system"]) for w in bench.WORKLOADS.values())
+
+
+def test_committed_bench_lines_carry_the_contract_keys():
+    """The evidence lines under profiles/ (written by bench.py on a B200) carry every key the bench
+    contract names: the base line, roofline (bound, achieved, peak, unit, frac, traffic), cpu_baseline
+    (value, unit, cores, kind, sample), e2e (value, unit, host<->device bytes), gpu_launches > 0 and
+    the clocks sampled under load; the reference arm's line is marked and self-consistent."""
+    import json
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    line = json.loads(open(os.path.join(root, "profiles", "r02_bench_default.json")).read().strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in line, k
+    assert line["n_gpus"] == 1 and line["warmup"] >= 3 and line["higher_is_better"] is True
+    assert line["config"]["workload"] == "lorenz3d" and "l2" in line["config"]
+    r = line["roofline"]
+    assert r["bound"] in ("hbm", "tensor", "alu") and r["frac"] == pytest.approx(r["achieved"] / r["peak"])
+    assert 0 < r["frac"] <= 1.0 and r["traffic"] > 0
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+    e = line["e2e"]
+    assert e["unit"] == line["unit"] and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert 0 < e["value"] < line["value"]
+    assert line["gpu_launches"] >= line["steps"]
+    clk = line["clocks"]
+    assert clk["sm_mhz"] > 0 and not set(clk["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    ref = json.loads(open(os.path.join(root, "profiles", "r02_bench_reference.json")).read().strip().splitlines()[-1])
+    assert ref["impl"] == "reference" and ref["metric"] == line["metric"] and ref["unit"] == line["unit"]
+    assert ref["config"]["workload"] == line["config"]["workload"]
+    assert ref["e2e"]["value"] == ref["value"] and ref["cpu_baseline"]["value"] == ref["value"]
