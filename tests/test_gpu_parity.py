@@ -694,3 +694,34 @@ def test_histogram_3d_random_cameras_and_magnitudes_bit_exact(seed, ppt, tpb):
     want = O.histogram(x, [0, 1, 2], M, W, H, 1, 0)
     got = ctx.read_image()
     assert np.array_equal(got, want), f"{np.count_nonzero(got != want)} pixels differ (kind {kind})"
+
+
+def test_swept_lorenz_lands_on_the_pitchfork_branches():
+    """Closed-form pin of the whole swept path (no oracle in the loop): configs[3]'s shape with r
+    Philox-swept over [0, 13) (2^20 particles, the bench's 4-per-thread kernel, 1000-step launches).
+    PAPER.md:89, :95: below r = 1 every particle goes to the origin (checked for r < 0.5); between the pitchfork and the
+    homoclinic r = 13.926 at C+- = (+-sqrt(8(r-1)/3), +-sqrt(8(r-1)/3), r - 1) -- each particle at the
+    fixed points of its OWN r (read back with ff_read_lifted), after 5000 RK4 steps."""
+    n = 1 << 20
+    ctx = lorenz_ctx([n])
+    g = ctx.init_group(LZ_LO, LZ_HI, n, 1, 0, seed=31)
+    ctx.sweep_param(g, "r", 0.0, 13.0, 0, seed=32)
+    for _ in range(5):
+        ctx.step(1000, 0.01)
+    x = ctx.read_state(g).astype(np.float64)
+    r = ctx.read_lifted(g).astype(np.float64)
+    assert np.array_equal(r.astype(np.float32), O.sweep_values(0.0, 13.0, 0, 32, 0, n, n))
+    low = r < 0.5          # (the origin's slowest rate, (sqrt(81 + 40 r) - 11) / 2, is -0.48 at r = 0.5)
+    assert low.sum() > 30000 and np.abs(x[:, low]).max() < 1e-3
+    mid = (r > 1.5) & (r < 12.5)
+    c = np.sqrt(8.0 / 3.0 * (r[mid] - 1.0))
+    assert mid.sum() > 700000
+    # (a particle starting next to the z axis -- the saddle's stable manifold -- lingers there for
+    # ln(1/distance) / 0.44 time units, so a handful of the 2^20 may still be on their way at t = 50)
+    dev = np.maximum(np.abs(np.abs(x[0, mid]) - c), np.abs(np.abs(x[1, mid]) - c)) / c
+    dev = np.maximum(dev, np.abs(x[2, mid] - (r[mid] - 1.0)) / (r[mid] - 1.0))
+    assert np.mean(dev < 1e-4) > 0.9999, np.sort(dev)[-10:]
+    assert np.all(np.sign(x[0, mid]) == np.sign(x[1, mid]))          # C+ or C-, never mixed
+    assert np.isfinite(x).all() and np.abs(x).max() < 60.0
+    both = np.mean(x[0, mid] > 0)
+    assert 0.3 < both < 0.7                                            # both branches populated
