@@ -245,3 +245,27 @@ def test_exchange_full_size_bench_launch(push):
         assert want.sum() > (1 << 22)          # both groups binned (the reset keeps the backward one in view)
         for _, img in ranks:
             assert np.array_equal(img.cpu().numpy().view(np.uint32), want)
+
+
+@pytest.mark.parametrize("push", [False, True])
+def test_exchanging_contexts_refuse_graph_capture(push):
+    """A captured frame would replay barrier values of the capture forever, so an exchanging context
+    (sum pass or push) refuses CUDA-graph capture with FF_ERR_STATE and stays usable afterwards."""
+    axes, view, shape = [0, 2], [-20.0, 20.0, 0.0, 50.0], (2, 16, 16)
+    ranks, streams, _ = (pushing_ranks if push else exchanged_ranks)(2, shape, axes, view)
+    frame(ranks, streams, 1)
+    ctx = ranks[0][0]
+    with pytest.raises(FFError) as e:
+        ctx.capture(lambda: ctx.step(1, 0.01))
+    assert e.value.status == FF_ERR_STATE
+    frame(ranks, streams, 1)                       # both ranks still exchange normally
+    want = np.zeros(shape, np.uint64)
+    for r in range(2):
+        c, im = make_rank(r, 2, shape, axes, view, grid_limit=0)
+        c.step(2, 0.01)
+        im.zero_()
+        c.step(0, 0.01)
+        c.sync()
+        want += im.cpu().numpy().view(np.uint32)
+    for _, img in ranks:
+        assert np.array_equal(img.cpu().numpy().view(np.uint32).astype(np.uint64), want)
