@@ -143,3 +143,26 @@ def test_config5_lorenz_1B_frame_image_is_oracle_histogram():
     assert np.array_equal(got, want), f"sums {int(got.sum())} vs {int(want.sum())}"
     assert int(want.astype(np.int64).sum()) > n // 4
     ctx.close()
+
+
+@pytest.mark.parametrize("name", ["lorenz3d", "stn_bif3d", "hh"])
+def test_run_to_run_bit_identical(name):
+    """Two independent contexts built by the bench's setup() run the same two frames: states, reset
+    counts and images are bit-identical (per-particle work is deterministic -- tile scheduling order
+    does not touch the arithmetic -- and integer counts commute)."""
+    w = bench.WORKLOADS[name]
+    runs = []
+    for _ in range(2):
+        ctx, gids, img, _ = bench.setup(ARGS, w, 0, 1)
+        for _ in range(2):
+            img.zero_()
+            ctx.step(w["S"], w["dt"])
+        ctx.sync()
+        runs.append(([ctx.read_state(g).view(np.uint32) for g in gids],
+                     [ctx.read_epochs(g) if "reset" in w else None for g in gids],
+                     img.cpu().numpy().copy()))
+        ctx.close()
+    (sa, ea, ia), (sb, eb, ib) = runs
+    assert all(np.array_equal(a, b) for a, b in zip(sa, sb))
+    assert all((a is None and b is None) or np.array_equal(a, b) for a, b in zip(ea, eb))
+    assert np.array_equal(ia, ib) and ia.sum() > 0
